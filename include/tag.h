@@ -1,0 +1,200 @@
+/*
+ * tag.h — C ABI of libtag: B200-native sufficient-factor-broadcasting (SFB) gradient
+ * synchronisation for replicated fully-connected / MatMul layers, the data-parallel hot path of
+ * TAG (Zhang et al., "Expediting Distributed DNN Training with Device Topology-Aware Graph
+ * Deployment", arXiv 2302.06126).
+ *
+ * Citations: P:n = line n of the paper's LaTeX source; S:n = line n of SPEC.md.
+ * DESIGN.md lists every reading taken where the paper is silent (R1..R19).
+ *
+ * The method (Fig. "fig:sfb_impl"): n data-parallel replicas of a Dense
+ * layer with weight W (M x N; M = input features = the paper's H1, N = output features = H2) each
+ * hold a batch shard of B rows. Replica r owns its sufficient factors
+ *     X_r  (B x M)  — the layer input x
+ *     dY_r (B x N)  — the gradient w.r.t. the output ∇
+ * Instead of all-reducing the M x N gradient, the factors are broadcast (all-gathered) to every
+ * replica and every replica reconstructs the identical gradient
+ *     dW = alpha * sum_{r<n} X_r^T dY_r = alpha * X_all^T dY_all,   K = n*B,  alpha = 1/(n*B)
+ * ("MatMul ops on each device can reconstruct identical gradients"; alpha: DESIGN R1).
+ *
+ * Conventions for every call below
+ *   - All matrices are dense, row-major, contiguous. Device pointers must be 16-byte aligned.
+ *   - dtype of X / dY = desc.in_dtype; of dW_out = desc.out_dtype. W and v are always fp32.
+ *   - Every call that takes a cudaStream_t is stream-ordered and asynchronous: it only enqueues
+ *     work; inputs must stay unmodified and all buffers alive until the stream passes the call.
+ *   - Ownership: the caller owns X, dY, dW_out, W, v and all host buffers. The plan owns its
+ *     gather buffers, staging buffers, TMA descriptors and NCCL reduction op; the comm owns the
+ *     NCCL communicator. Destroy plans before their comm.
+ *   - Collective calls (marked COLLECTIVE) must be made by every rank of the comm, in the same
+ *     order, with identical descriptors — the NCCL rule.
+ *   - Errors: argument validation happens on the host before anything is enqueued; an invalid
+ *     argument returns TAG_ERR_INVALID_ARG with no side effects. CUDA / NCCL failures return
+ *     TAG_ERR_CUDA / TAG_ERR_NCCL; an asynchronous NCCL error detected on entry returns
+ *     TAG_ERR_ASYNC. tag_last_error() gives a thread-local human-readable detail. Nothing throws
+ *     across the ABI. There is no CPU fallback: without a usable CUDA device every compute call
+ *     fails with TAG_ERR_CUDA.
+ */
+#ifndef TAG_H_
+#define TAG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* tag_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    TAG_OK = 0,
+    TAG_ERR_INVALID_ARG = 1,
+    TAG_ERR_UNSUPPORTED = 2,
+    TAG_ERR_CUDA = 3,
+    TAG_ERR_NCCL = 4,
+    TAG_ERR_OOM = 5,
+    TAG_ERR_NOT_INITIALIZED = 6,
+    TAG_ERR_ASYNC = 7
+} tag_status_t;
+
+typedef enum { TAG_F32 = 0, TAG_BF16 = 1 } tag_dtype_t;
+
+/* Per-layer synchronisation choice: Replicate-with-AllReduce, or SFB
+ * ("Duplicate" of the gradient op, P:363-365 / P:523-524); NONE when n = 1. */
+typedef enum { TAG_SYNC_ALLREDUCE = 0, TAG_SYNC_SFB = 1, TAG_SYNC_NONE = 2 } tag_choice_t;
+
+/* Readings of the SFB communication term (DESIGN R2): north_star's gathered bytes n*S (default),
+ * the paper ILP's D(D-1)*S broadcast term, or the physical all-gather wire (n-1)*S. */
+typedef enum { TAG_RULE_NORTHSTAR = 0, TAG_RULE_PAPER_ILP = 1, TAG_RULE_WIRE = 2 } tag_rule_t;
+
+typedef struct tag_comm_s* tag_comm_t;
+typedef struct tag_plan_s* tag_sfb_plan_t;
+
+/* ------------------------------------------------------------------------------------------ */
+/* Library info                                                                               */
+/* ------------------------------------------------------------------------------------------ */
+const char* tag_version(void);
+const char* tag_status_string(tag_status_t s);
+/* Detail of the last error raised on the calling thread ("" if none). Valid until the next call. */
+const char* tag_last_error(void);
+/* Number of libtag kernels launched by this process so far (all plans, all streams). */
+uint64_t tag_kernel_launches(void);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Communicator bootstrap (one process per GPU, P:716-718 NCCL; DESIGN "Multi-GPU")           */
+/* ------------------------------------------------------------------------------------------ */
+/* Rank 0 creates a 128-byte id (ncclGetUniqueId); the caller broadcasts it to every rank with
+ * its own transport (torch.distributed in the Python binding). */
+tag_status_t tag_get_unique_id(unsigned char id[128]);
+/* COLLECTIVE. Sets the CUDA device to `cuda_device` for the calling thread and creates the NCCL
+ * communicator of `nranks` ranks. nranks == 1 is valid and creates no NCCL communicator (`id` may
+ * be NULL then). *out is set only on success. */
+tag_status_t tag_comm_create(const unsigned char id[128], int nranks, int rank, int cuda_device,
+                             tag_comm_t* out);
+/* COLLECTIVE. Destroys the communicator. NULL is a no-op. */
+tag_status_t tag_comm_destroy(tag_comm_t comm);
+tag_status_t tag_comm_info(tag_comm_t comm, int* nranks, int* rank, int* cuda_device);
+
+/* ------------------------------------------------------------------------------------------ */
+/* SFB plan: one replicated Dense layer                                                       */
+/* ------------------------------------------------------------------------------------------ */
+typedef struct {
+    int64_t M;               /* input features (H1); rows of dW                      */
+    int64_t N;               /* output features (H2); columns of dW                  */
+    int64_t B;               /* rows (samples / tokens) per replica                         */
+    int n;                   /* replicas; must equal the comm size                          */
+    tag_dtype_t in_dtype;    /* dtype of X and dY as the caller holds them                  */
+    tag_dtype_t wire_dtype;  /* dtype of the broadcast factors: F32->F32, BF16->BF16 or     */
+                             /* F32->BF16 (RNE cast in the pack kernel, DESIGN R11)         */
+    tag_dtype_t out_dtype;   /* dtype of dW_out (F32 default; BF16 = RNE of the fp32 value) */
+    int fuse_sgd;            /* 1: tag_sfb_sync_sgd applies SGD-momentum in the epilogue    */
+    float lr, momentum, weight_decay; /* SGD hyper-parameters, frozen in the plan (R14)     */
+} tag_sfb_desc_t;
+
+/* COLLECTIVE. Validates `desc`, allocates the gather buffers (n*B*M and n*B*N elements of the
+ * wire dtype) and staging, and creates the PreMulSum(1/(nB)) NCCL op used by the dense path.
+ * Errors: TAG_ERR_INVALID_ARG (bad dims/dtypes, n != comm size), TAG_ERR_OOM, TAG_ERR_NCCL. */
+tag_status_t tag_sfb_plan(tag_comm_t comm, const tag_sfb_desc_t* desc, tag_sfb_plan_t* out);
+/* COLLECTIVE. NULL is a no-op. The caller must ensure no work using the plan is still pending. */
+tag_status_t tag_sfb_plan_destroy(tag_sfb_plan_t plan);
+
+/* COLLECTIVE (n > 1). The SFB synchronisation of one layer, steps a1-a4:
+ *   a1 pack   : if in_dtype != wire_dtype, RNE-cast X_r and dY_r into this rank's slot of the
+ *               gather buffers (16-byte vectorised kernel);
+ *   a2 gather : NCCL all-gather of X_r and dY_r over NVLink ("broadcast to all devices");
+ *   a3 recon  : dW = alpha * X_all^T dY_all on the tensor cores (K = n*B), alpha = 1/(nB);
+ *   a4 store  : dW_out <- dW in out_dtype (fused epilogue).
+ * X: B x M, dY: B x N (in_dtype, device). dW_out: M x N (out_dtype, device), overwritten.
+ * dW_out is bitwise identical on every rank. n = 1: a3-a4 only, alpha = 1/B. */
+tag_status_t tag_sfb_sync(tag_sfb_plan_t plan, const void* X, const void* dY, void* dW_out,
+                          tag_stream_t stream);
+
+/* Stage split of tag_sfb_sync for staged timing: gather = a1 + a2 into the plan's gather
+ * buffers (COLLECTIVE for n > 1); reconstruct = a3 + a4 from the most recent gather on the same
+ * stream. tag_sfb_gather followed by tag_sfb_reconstruct == tag_sfb_sync. */
+tag_status_t tag_sfb_gather(tag_sfb_plan_t plan, const void* X, const void* dY,
+                            tag_stream_t stream);
+tag_status_t tag_sfb_reconstruct(tag_sfb_plan_t plan, void* dW_out, tag_stream_t stream);
+
+/* COLLECTIVE (n > 1). tag_sfb_sync with the optimizer op fused into the reconstruction epilogue
+ * (the ApplyGradient op l that consumes the gradient; SGD-momentum per R14):
+ *   g = dW + wd*W ; v <- momentum*v + g ; W <- W - lr*v        (W, v: M x N fp32, in place)
+ * dW_out may be NULL (then dW is never written to HBM). Requires desc.fuse_sgd = 1. */
+tag_status_t tag_sfb_sync_sgd(tag_sfb_plan_t plan, const void* X, const void* dY, float* W,
+                              float* v, void* dW_out, tag_stream_t stream);
+
+/* COLLECTIVE (n > 1). End-to-end form with HOST buffers: copies X and dY (pinned or pageable
+ * host memory, in_dtype) to plan-owned device staging, runs tag_sfb_sync into plan-owned device
+ * memory and copies dW (out_dtype) back to dW_host. Stream-ordered like the others: the host
+ * buffers are read / written when the stream reaches the copies. */
+tag_status_t tag_sfb_sync_host(tag_sfb_plan_t plan, const void* X_host, const void* dY_host,
+                               void* dW_host, tag_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Dense-gradient baseline ("Replicate with AllReduce")                 */
+/* ------------------------------------------------------------------------------------------ */
+/* Local, unscaled gradient of this replica: dW_local = X_r^T dY_r (K = B) in out_dtype, operands
+ * cast to wire_dtype first (same tensor-core path as the reconstruction). Not collective. */
+tag_status_t tag_local_grad(tag_sfb_plan_t plan, const void* X, const void* dY, void* dW_local,
+                            tag_stream_t stream);
+/* COLLECTIVE. In place: dW <- (1/(nB)) * sum_ranks dW, one ncclAllReduce whose PreMulSum op
+ * applies the scale inside the collective (P:566 ring AllReduce). dW: M x N out_dtype.
+ * n = 1: dW <- dW / B. */
+tag_status_t tag_dense_allreduce(tag_sfb_plan_t plan, void* dW, tag_stream_t stream);
+/* Unfused optimizer step of the dense path (same arithmetic as the fused epilogue):
+ * g = dW + wd*W; v <- momentum*v + g; W <- W - lr*v. dW fp32 (out_dtype must be F32). */
+tag_status_t tag_sgd_step(tag_sfb_plan_t plan, const float* dW, float* W, float* v,
+                          tag_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Selector: per-layer SFB vs AllReduce (the paper's SFB ILP, for one MatMul cut)  */
+/* ------------------------------------------------------------------------------------------ */
+typedef struct {
+    int64_t M, N, B;          /* layer dims and rows per replica                              */
+    tag_dtype_t factor_dtype; /* e_w: bytes per factor element on the wire                    */
+    tag_dtype_t grad_dtype;   /* e_g: bytes per gradient element the dense path all-reduces   */
+} tag_layer_t;
+
+typedef struct {
+    int n;                     /* replicas D                                           */
+    uint64_t link_bytes_per_s; /* tau: bottleneck bandwidth between the D devices     */
+    uint64_t tensor_flops;     /* F: T_g = 2*M*N*B / F (linear model P:326-328); 0 = ignore   */
+    int rule;                  /* tag_rule_t                                                   */
+} tag_topology_t;
+
+/* Host only; no device or communicator work. For each layer i, out[i] is
+ *   TAG_SYNC_NONE      if n <= 1;
+ *   TAG_SYNC_SFB       iff (n-1)*T_g + c_rule*S/tau < 2(n-1)/n * G/tau  strictly, with
+ *                      S = B(M+N)e_w, G = M*N*e_g, c_rule = n | n(n-1) | n-1 (R2, R4);
+ *   TAG_SYNC_ALLREDUCE otherwise (ties keep AllReduce).
+ * Evaluated exactly in 128-bit integers after clearing denominators (R4c), so the decision is
+ * bit-exact and identical on every rank. Errors: TAG_ERR_INVALID_ARG for NULL pointers,
+ * num_layers < 0, non-positive dims, tau = 0, or an unknown rule/dtype; TAG_ERR_UNSUPPORTED if
+ * an intermediate would overflow 127 bits. */
+tag_status_t tag_sfb_select(const tag_layer_t* layers, int num_layers, const tag_topology_t* topo,
+                            tag_choice_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAG_H_ */

@@ -1,0 +1,263 @@
+"""Pins for the CPU oracle (`-m "not gpu"`): the oracle is checked against things other than itself —
+values the paper/SPEC print, closed forms, invariants, exact-rational brute force, and textbook
+library routines — so that a dropped term, wrong sign/index or transposed operand fails a test.
+"""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2302_06126_b200 import synth
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+SHAPES = [(1, 1, 1, 2), (3, 5, 2, 3), (17, 33, 3, 4), (64, 32, 4, 2), (130, 257, 5, 2)]  # (M,N,B,n)
+
+
+def _rel_fro(a, r):
+    return np.linalg.norm(a - r) / np.linalg.norm(r)
+
+
+def _inputs(M, N, B, n, dist="normal", cid=900):
+    return synth.all_factors(cid, M * 1000 + N, n, M, N, B, dist, dist)
+
+
+# ---------------------------------------------------------------------------------------------
+# Lossless: SFB reconstruction == dense AllReduce result
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("M,N,B,n", SHAPES)
+def test_lossless_random(oracle_mod, M, N, B, n):
+    X, dY = _inputs(M, N, B, n)
+    d, s = oracle_mod.dense_dw(X, dY), oracle_mod.sfb_dw(X, dY)
+    assert _rel_fro(s, d) <= 1e-13
+
+
+@pytest.mark.parametrize("M,N,B,n", SHAPES)
+def test_lossless_integers_exact(oracle_mod, M, N, B, n):
+    X, dY = _inputs(M, N, B, n, "int3")
+    assert np.array_equal(oracle_mod.dense_sum(X, dY), oracle_mod.sfb_sum(X, dY))
+    assert np.array_equal(oracle_mod.dense_dw(X, dY), oracle_mod.sfb_dw(X, dY))
+
+
+# ---------------------------------------------------------------------------------------------
+# Brute force with exact rationals (P:520-526 definition written out element by element)
+# ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("M,N,B,n", [(1, 1, 1, 2), (3, 5, 2, 3), (4, 3, 3, 2)])
+@pytest.mark.parametrize("dist", ["int3", "normal"])
+def test_bruteforce_fractions(oracle_mod, M, N, B, n, dist):
+    X, dY = _inputs(M, N, B, n, dist)
+    got = oracle_mod.sfb_dw(X, dY)
+    got_dense = oracle_mod.dense_dw(X, dY)
+    for m in range(M):
+        for j in range(N):
+            exact = sum(Fraction(float(X[r, b, m])) * Fraction(float(dY[r, b, j]))
+                        for r in range(n) for b in range(B)) / (n * B)
+            if dist == "int3":
+                # K <= 6 products of small integers: the fp64 sum is exact; /nB rounds once
+                assert got[m, j] == float(exact) and got_dense[m, j] == float(exact)
+            else:
+                assert abs(Fraction(got[m, j]) - exact) <= abs(exact) * Fraction(1, 2 ** 48) + \
+                    Fraction(1, 2 ** 60)
+
+
+def test_fixture_shapes_against_fractions_integer_sum(oracle_mod):
+    """(130,257,5,2) and (17,33,3,4): non-power-of-two nB and odd tiles; integer sums exact."""
+    for (M, N, B, n) in [(17, 33, 3, 4), (130, 257, 5, 2)]:
+        X, dY = _inputs(M, N, B, n, "int3")
+        S = oracle_mod.sfb_sum(X, dY)
+        Xi, dYi = X.astype(np.int64), dY.astype(np.int64)
+        exact = np.zeros((M, N), dtype=np.int64)
+        for r in range(n):
+            exact += Xi[r].T @ dYi[r]          # integer matmul: exact
+        assert np.array_equal(S, exact.astype(np.float64))
+
+
+# ---------------------------------------------------------------------------------------------
+# Textbook reductions
+# ---------------------------------------------------------------------------------------------
+def test_n1_reduces_to_matmul(oracle_mod):
+    """n = 1: dW = (1/B) X^T dY — checked against torch.matmul in fp64 (a library routine)."""
+    X, dY = _inputs(96, 80, 7, 1)
+    ref = (torch.from_numpy(X[0]).double().T @ torch.from_numpy(dY[0]).double()).numpy() / 7
+    assert _rel_fro(oracle_mod.sfb_dw(X, dY), ref) <= 1e-14
+
+
+def test_dense_sum_is_sum_of_replica_products(oracle_mod):
+    X, dY = _inputs(40, 24, 6, 3)
+    ref = sum(X[r].astype(np.float64).T @ dY[r].astype(np.float64) for r in range(3))
+    assert _rel_fro(oracle_mod.dense_sum(X, dY), ref) <= 1e-14
+    # orientation pin: dW[m][j] pairs input feature m with output feature j
+    m, j = 7, 19
+    direct = sum(float(X[r, b, m]) * float(dY[r, b, j]) for r in range(3) for b in range(6))
+    assert abs(oracle_mod.dense_sum(X, dY)[m, j] - direct) <= 1e-12 * max(1.0, abs(direct))
+
+
+def test_scale_ones(oracle_mod):
+    """X = 1, dY = 1 -> every entry of the (1/(nB))-scaled gradient is exactly 1."""
+    for (M, N, B, n) in [(5, 3, 3, 3), (64, 32, 4, 2), (8, 8, 7, 5)]:
+        X = np.ones((n, B, M), np.float32)
+        dY = np.ones((n, B, N), np.float32)
+        assert np.all(oracle_mod.sfb_dw(X, dY) == 1.0)
+        assert np.all(oracle_mod.dense_dw(X, dY) == 1.0)
+
+
+def test_scale_is_global_batch_mean(oracle_mod):
+    """Replicating one replica's factors n times leaves the mean gradient unchanged (alpha=1/(nB))."""
+    X, dY = _inputs(12, 10, 4, 1, "int3")
+    one = oracle_mod.sfb_dw(X, dY)
+    rep = oracle_mod.sfb_dw(np.repeat(X, 4, axis=0), np.repeat(dY, 4, axis=0))
+    assert np.array_equal(one, rep)
+
+
+def test_rank_bound(oracle_mod):
+    """rank(dW) <= nB (the gradient is the product of two smaller matrices); Gaussian
+    factors with nB < min(M, N) give rank exactly nB."""
+    X, dY = _inputs(64, 32, 4, 2)
+    s = np.linalg.svd(oracle_mod.sfb_dw(X, dY), compute_uv=False)
+    assert s[8] / s[0] < 1e-12
+    assert s[7] / s[0] > 1e-6
+
+
+def test_entries_match_full(oracle_mod):
+    X, dY = _inputs(130, 257, 5, 2)
+    full = oracle_mod.sfb_sum(X, dY)
+    idx = np.random.default_rng(0).integers(0, 130 * 257, 300)
+    assert np.array_equal(oracle_mod.sfb_sum_entries(X, dY, idx), full.ravel()[idx])
+
+
+# ---------------------------------------------------------------------------------------------
+# SGD-momentum (R14): closed form for a constant gradient
+# ---------------------------------------------------------------------------------------------
+def test_sgd_closed_form(oracle_mod):
+    g = np.random.default_rng(1).standard_normal((6, 5))
+    W0 = np.random.default_rng(2).standard_normal((6, 5))
+    W, v = W0.copy(), np.zeros_like(W0)
+    lr, mu, k = 0.05, 0.9, 7
+    for _ in range(k):
+        W, v = oracle_mod.sgd_momentum(g, W, v, lr, mu, 0.0)
+    vk = g * (1 - mu ** k) / (1 - mu)
+    Wk = W0 - lr * g * sum((1 - mu ** j) / (1 - mu) for j in range(1, k + 1))
+    assert np.allclose(v, vk, rtol=1e-13, atol=1e-15)
+    assert np.allclose(W, Wk, rtol=1e-13, atol=1e-15)
+
+
+def test_sgd_weight_decay_folds_into_gradient(oracle_mod):
+    rs = np.random.default_rng(3)
+    g, W0, v0 = rs.standard_normal((4, 4)), rs.standard_normal((4, 4)), rs.standard_normal((4, 4))
+    a = oracle_mod.sgd_momentum(g, W0, v0, 0.1, 0.5, 0.01)
+    b = oracle_mod.sgd_momentum(g + 0.01 * W0, W0, v0, 0.1, 0.5, 0.0)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    # mu = 0, wd = 0 is plain gradient descent W - lr*g (P:283 GradientDescent)
+    c = oracle_mod.sgd_momentum(g, W0, v0, 0.1, 0.0, 0.0)
+    assert np.allclose(c[0], W0 - 0.1 * g, rtol=0, atol=1e-15)
+
+
+# ---------------------------------------------------------------------------------------------
+# RNE fp32 -> bf16 cast (R11), pinned to torch's CPU conversion (a library routine)
+# ---------------------------------------------------------------------------------------------
+def test_bf16_rne_matches_torch(oracle_mod):
+    rs = np.random.default_rng(4)
+    x = np.concatenate([
+        rs.standard_normal(100000).astype(np.float32),
+        (rs.standard_normal(1000) * 1e-38).astype(np.float32),            # subnormals
+        np.array([0.0, -0.0, np.inf, -np.inf, 3.4e38, -3.4e38, 1.0, 1 + 2 ** -8, 1 + 3 * 2 ** -8,
+                  1 + 2 ** -9, 1 + 3 * 2 ** -9], np.float32),               # exact ties, both ways
+    ])
+    ours = oracle_mod.cast_bf16_bits(x)
+    ref = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+    assert np.array_equal(ours, ref)
+    nan = oracle_mod.cast_bf16_bits(np.array([np.nan], np.float32))
+    assert np.isnan(oracle_mod.bf16_bits_to_f64(nan)[0])
+
+
+def test_bf16_tie_rounds_to_even(oracle_mod):
+    # 1 + 2^-8 is exactly half-way between bf16 1.0 and 1 + 2^-7: even mantissa (1.0) wins
+    assert oracle_mod.bf16_bits_to_f64(oracle_mod.cast_bf16_bits(
+        np.array([1 + 2 ** -8], np.float32)))[0] == 1.0
+    assert oracle_mod.bf16_bits_to_f64(oracle_mod.cast_bf16_bits(
+        np.array([1 + 3 * 2 ** -8], np.float32)))[0] == 1 + 2 ** -6
+
+
+# ---------------------------------------------------------------------------------------------
+# Byte counts, ring AllReduce, ILP objective (golden values printed by the paper / SPEC)
+# ---------------------------------------------------------------------------------------------
+def _golden(name):
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+def test_spec_volume_fixture(oracle_mod):
+    g = _golden("spec_volume.json")
+    S = oracle_mod.selector
+    assert S.sfb_elements_fig5(g["H1"], g["H2"], g["B"]) == g["sfb_elements"]
+    assert S.gradient_elements(g["H1"], g["H2"]) == g["gradient_elements"]
+    assert g["gradient_elements"] // g["sfb_elements"] == g["reduction"]
+    # north_star's gathered-bytes count coincides with Fig. 5 at D = 2 (R2), in elements
+    assert S.sfb_gathered_bytes(g["D"], g["B"], g["H1"], g["H2"], 1) == g["sfb_elements"]
+    # and the all-gather wire per rank is half of it at D = 2
+    assert S.allgather_ingress_bytes(2, 4, 256, 256, 1) == 2048
+
+
+def test_spec_ring_allreduce(oracle_mod):
+    for c in _golden("spec_ring_allreduce.json")["cases"]:
+        t = oracle_mod.selector.ring_allreduce_time(c["D"], c["size_bytes"], c["tau"])
+        assert t == Fraction(c["seconds"])
+
+
+def test_spec_ilp_objective(oracle_mod):
+    S = oracle_mod.selector
+    c1, c2 = _golden("spec_sfb_ilp.json")["cases"]
+    obj = S.ilp_objective(c1["D"], Fraction(c1["T_g"]), c1["cut_bytes"], c1["L_gl"], c1["tau"])
+    assert obj == Fraction(c1["objective"])
+    L = c1["as_layer"]
+    layer = dict(M=L["M"], N=L["N"], B=L["B"], e_w=L["e_w"], e_g=L["e_g"])
+    topo = dict(n=2, tau=c1["tau"], F=L["F"], rule=S.RULE_PAPER_ILP)
+    sfb, ar = S.sfb_cost_terms(layer, topo)
+    assert sfb - ar == Fraction(c1["objective"])
+    for rule in (S.RULE_PAPER_ILP, S.RULE_NORTHSTAR, S.RULE_WIRE):
+        assert S.select(layer, dict(topo, rule=rule)) == S.CHOICE_SFB
+    # WIRE reading at D = 2: (n-1) S / tau instead of n(n-1) S / tau -> -9.8e-4
+    sfb, ar = S.sfb_cost_terms(layer, dict(topo, rule=S.RULE_WIRE))
+    assert sfb - ar == Fraction("-9.8e-4")
+    # second SPEC case: cut == gradient size, zero compute, D = 2 -> keep AllReduce (alpha = 0)
+    assert S.ilp_objective(2, 0, c2["cut_bytes"], c2["L_gl"], c2["tau"]) > 0
+    layer2 = dict(M=1000, N=1000, B=1, e_w=500, e_g=1)      # S = 1e6 B = G, T_g dropped (F = 0)
+    assert S.select(layer2, dict(n=2, tau=c2["tau"], F=0, rule=S.RULE_PAPER_ILP)) == \
+        S.CHOICE_ALLREDUCE
+
+
+def test_selector_n1_and_tie(oracle_mod):
+    S = oracle_mod.selector
+    lay = dict(M=16, N=16, B=4, e_w=2, e_g=2)
+    assert S.select(lay, dict(n=1, tau=1, F=0)) == S.CHOICE_NONE
+    # exact tie: n^2 S = 4*256 = 1024 = 2 (n-1) G -> AllReduce
+    sfb, ar = S.sfb_cost_terms(lay, dict(n=2, tau=10 ** 9, F=0))
+    assert sfb == ar
+    assert S.select(lay, dict(n=2, tau=10 ** 9, F=0)) == S.CHOICE_ALLREDUCE
+    assert S.select(dict(lay, B=3), dict(n=2, tau=10 ** 9, F=0)) == S.CHOICE_SFB
+
+
+def test_selector_integer_form_equals_fraction_form(oracle_mod):
+    S = oracle_mod.selector
+    rs = np.random.default_rng(5)
+    for _ in range(3000):
+        lay = dict(M=int(rs.integers(1, 40000)), N=int(rs.integers(1, 40000)),
+                   B=int(rs.integers(1, 600)), e_w=int(rs.choice([2, 4])),
+                   e_g=int(rs.choice([2, 4])))
+        topo = dict(n=int(rs.integers(1, 17)), tau=int(rs.integers(1, 10 ** 12)),
+                    F=int(rs.choice([0, int(rs.integers(1, 3 * 10 ** 15))])),
+                    rule=int(rs.integers(0, 3)))
+        assert S.select(lay, topo) == S.select_integer_form(lay, topo)
+
+
+def test_appendix_a_decision_table(oracle_mod):
+    S = oracle_mod.selector
+    name = {S.CHOICE_ALLREDUCE: "AR", S.CHOICE_SFB: "SFB", S.CHOICE_NONE: "NONE"}
+    cases = _golden("appendix_a_decisions.json")["cases"]
+    assert len(cases) == 200
+    for c in cases:
+        lay = dict(M=c["M"], N=c["N"], B=c["B"], e_w=c["e_w"], e_g=c["e_g"])
+        topo = dict(n=c["n"], tau=c["tau"], F=c["F"], rule=c["rule"])
+        assert name[S.select(lay, topo)] == c["expect"], c
