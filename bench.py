@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""bench.py — per-layer SFB gradient synchronisation on B200 (TAG, arXiv 2302.06126).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU, NCCL)
+
+Workload (BASELINE.json configs[1]): VGG-19 fc6 / fc7 / fc8 (25088x4096, 4096x4096, 4096x1000),
+B = 32 rows per GPU, bf16 factors in and on the wire, fp32 dW out; n = N replicas. One STEP =
+the whole hot path for every layer: pack (when a cast is needed) -> NCCL all-gather of the
+factors (n > 1) -> tensor-core reconstruction of dW with the fused 1/(nB) scale; the selector is
+evaluated per layer (host, exact integers). Synthetic seeded data (paper_2302_06126_b200/synth.py).
+
+metric "dW GB/s": dW bytes materialised by all replicas per second = n * sum_layers M*N*4 / t_step
+(each replica reconstructs the identical gradient). Device-timed with CUDA events on
+the launching stream, max over ranks; L2 flushed (256 MiB write) between timed steps, outside the
+timed interval. Per-layer sync us, stage split, roofline of the reconstruction kernel, the e2e
+number through the host-buffer C-ABI call, clocks and the CPU-oracle baseline are in the same line.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2302_06126_b200 import dist as tdist  # noqa: E402
+from paper_2302_06126_b200 import synth  # noqa: E402
+
+METRIC = "per-layer SFB grad-sync us & dW GB/s (VGG-19 fc6/fc7/fc8, B=32/GPU)"
+ESIZE = {"f32": 4, "bf16": 2}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return pk, "measured (MEASURED_PEAKS.json)"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_oracle_baseline(cfg, n, budget_mac=2.5e10):
+    """Time the fp64 CPU oracle (as it stands) on a bounded sample of the same workload: the first
+    M_s input-feature rows of every layer's dW, M_s scaled so the sample is ~budget_mac MACs."""
+    import oracle
+    oracle.build()
+    cores = os.cpu_count()
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    total_bytes, total_t, desc = 0, 0.0, []
+    full_mac = sum(L.M * L.N * n * L.B for L in cfg.layers)
+    frac = min(1.0, budget_mac / full_mac)
+    for li, L in enumerate(cfg.layers):
+        Ms = max(8, int(L.M * frac))
+        X, dY = synth.all_factors(cfg.cid, li, n, L.M, L.N, L.B, L.x_dist, L.dy_dist)
+        Xs = torch.from_numpy(np.ascontiguousarray(X[:, :, :Ms])).to(torch.bfloat16).double().numpy()
+        dYe = torch.from_numpy(dY).to(torch.bfloat16).double().numpy()
+        t0 = time.perf_counter()
+        oracle.sfb_dw(Xs, dYe)
+        total_t += time.perf_counter() - t0
+        total_bytes += Ms * L.N * ESIZE[cfg.out_dtype]
+        desc.append(f"{L.name}:{Ms}/{L.M} rows")
+    return {"value": total_bytes / total_t / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "seconds": round(total_t, 3),
+            "sample": f"fp64 SFB route, n={n}, K={n * cfg.layers[0].B}, dW rows " + ", ".join(desc)}
+
+
+def run_reference(args, cfg, rank, world):
+    """--impl reference: the CPU oracle (this tier's reference arm) on the same config/metric."""
+    if rank != 0:
+        return
+    n = world
+    vals = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_oracle_baseline(cfg, n, budget_mac=args.ref_mac)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "ms_per_step": None, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_json(cfg, n, args),
+            "cpu_baseline": dict(cb, value=v),
+            "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "CPU fp64 oracle on the host cores, one replica's dW per step (bounded sample)"}
+    print(json.dumps(line), flush=True)
+
+
+def config_json(cfg, n, args):
+    return {"workload": f"{cfg.name} sync (configs[{cfg.cid - 1}]), n={n}",
+            "layers": [f"{L.name} {L.M}x{L.N}" for L in cfg.layers], "rows_per_gpu": cfg.layers[0].B,
+            "n": n, "in/wire/out": f"{cfg.in_dtype}/{cfg.wire_dtype}/{cfg.out_dtype}",
+            "parallelism": f"dp{n} (SFB all-gather + replicated reconstruction)",
+            "l2": "flushed between timed steps (256 MiB write), outside the timed interval"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="tag", choices=["tag", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dense", action="store_true")
+    ap.add_argument("--ref-mac", type=float, default=2.5e10)
+    args = ap.parse_args()
+    assert args.warmup >= 3 or args.impl == "reference", "need >= 3 warm-up steps"
+
+    rank, local_rank, world = tdist.init_from_env()
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+
+    from paper_2302_06126_b200 import tag
+    torch.cuda.set_device(local_rank)
+    n = world
+    comm = tdist.bootstrap_comm(tag, local_rank)
+    stream = torch.cuda.Stream()
+    tdt = {"f32": torch.float32, "bf16": torch.bfloat16}
+    layers = []
+    for li, L in enumerate(cfg.layers):
+        X, dY = synth.factors(cfg.cid, li, rank, L.M, L.N, L.B, L.x_dist, L.dy_dist)
+        plan = tag.SfbPlan(comm, L.M, L.N, L.B, cfg.in_dtype, cfg.wire_dtype, cfg.out_dtype)
+        Xh = torch.from_numpy(X).to(tdt[cfg.in_dtype]).pin_memory()
+        dYh = torch.from_numpy(dY).to(tdt[cfg.in_dtype]).pin_memory()
+        layers.append(dict(L=L, plan=plan, X=Xh.cuda(), dY=dYh.cuda(), Xh=Xh, dYh=dYh,
+                           dW=torch.empty(L.M, L.N, dtype=tdt[cfg.out_dtype], device="cuda")))
+    peaks, peak_src = load_peaks()
+    choices = tag.select([dict(M=l["L"].M, N=l["L"].N, B=l["L"].B, factor_dtype=cfg.wire_dtype,
+                               grad_dtype=cfg.out_dtype) for l in layers], n,
+                         900_000_000_000, int(peaks.get("bf16_tflops_sustained", 1400) * 1e12))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    nl = len(layers)
+
+    def step(evs=None):
+        with torch.cuda.stream(stream):
+            for i, l in enumerate(layers):
+                if evs is None:
+                    l["plan"].sync(l["X"], l["dY"], l["dW"], stream)
+                else:
+                    l["plan"].gather(l["X"], l["dY"], stream)
+                    evs[2 * i + 1].record(stream)
+                    l["plan"].reconstruct(l["dW"], stream)
+                    evs[2 * i + 2].record(stream)
+
+    def timed_loop(nsteps, staged):
+        per_step, per_layer_recon, per_layer_sync = [], [[] for _ in range(nl)], [[] for _ in range(nl)]
+        for _ in range(nsteps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            tdist.barrier()
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nl + 1)]
+            evs[0].record(stream)
+            step(evs if staged else None)
+            if not staged:
+                evs[-1].record(stream)
+            torch.cuda.synchronize()
+            per_step.append(evs[0].elapsed_time(evs[-1 if not staged else 2 * nl]))
+            if staged:
+                for i in range(nl):
+                    per_layer_recon[i].append(evs[2 * i + 1].elapsed_time(evs[2 * i + 2]))
+                    per_layer_sync[i].append(evs[2 * i].elapsed_time(evs[2 * i + 2]))
+        return per_step, per_layer_recon, per_layer_sync
+
+    # ---------------------------------------------------------------- warm-up + timed region
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    tdist.barrier()
+    launches0 = tag.kernel_launches()
+    with ClockSampler(local_rank) as clk:
+        steps_ms, recon_ms, sync_ms = timed_loop(args.steps, staged=True)
+    launches = tag.kernel_launches() - launches0
+    torch.cuda.synchronize()
+    tdist.barrier()
+
+    mean_step = statistics.mean(steps_ms)
+    t_step_ms = tdist.max_over_ranks(mean_step)
+    dw_bytes = sum(l["L"].M * l["L"].N * ESIZE[cfg.out_dtype] for l in layers)
+    value = n * dw_bytes / (t_step_ms * 1e-3) / 1e9
+
+    # roofline of the dominant kernel: the reconstruction (recon_tc_kernel), HBM-bound here
+    alg_bytes = sum(n * l["L"].B * (l["L"].M + l["L"].N) * ESIZE[cfg.wire_dtype]
+                    + l["L"].M * l["L"].N * ESIZE[cfg.out_dtype] for l in layers)
+    recon_mean_ms = [statistics.mean(r) for r in recon_ms]
+    recon_total_ms = tdist.max_over_ranks(sum(recon_mean_ms))
+    achieved = alg_bytes / (recon_total_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "recon_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"config{args.config}_n{n}")
+        except Exception:
+            traffic = None
+    roofline = {"kernel": "recon_tc_kernel (tcgen05 reconstruction + fused 1/(nB) epilogue)",
+                "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_step": alg_bytes,
+                "recon_share_of_step": round(recon_total_ms / t_step_ms, 3)}
+
+    per_layer = {}
+    for i, l in enumerate(layers):
+        L = l["L"]
+        t_sync = tdist.max_over_ranks(statistics.median(sync_ms[i]))
+        t_rec = tdist.max_over_ranks(statistics.median(recon_ms[i]))
+        flops = 2.0 * L.M * L.N * n * L.B
+        rbytes = n * L.B * (L.M + L.N) * ESIZE[cfg.wire_dtype] + L.M * L.N * ESIZE[cfg.out_dtype]
+        ag = (n - 1) * L.B * (L.M + L.N) * ESIZE[cfg.wire_dtype]
+        per_layer[L.name] = {
+            "sync_us": round(t_sync * 1e3, 2), "recon_us": round(t_rec * 1e3, 2),
+            "gather_us": round((t_sync - t_rec) * 1e3, 2),
+            "dW_GBps": round(L.M * L.N * ESIZE[cfg.out_dtype] / (t_sync * 1e-3) / 1e9, 1),
+            "recon_hbm_frac": round(rbytes / (t_rec * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+            "recon_tensor_frac": round(flops / (t_rec * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
+            "allgather_busbw_GBps": round(ag / ((t_sync - t_rec) * 1e-3) / 1e9, 1) if n > 1 else None,
+            "selector": {0: "allreduce", 1: "sfb", 2: "none"}[choices[i]]}
+
+    # ---------------------------------------------------------------- dense baseline (n > 1)
+    if n > 1 and not args.no_dense:
+        for i, l in enumerate(layers):
+            L = l["L"]
+            t = []
+            for _ in range(max(3, min(args.steps, 10))):
+                flush.zero_()
+                torch.cuda.synchronize()
+                tdist.barrier()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                l["plan"].local_grad(l["X"], l["dY"], l["dW"], stream)
+                l["plan"].dense_allreduce(l["dW"], stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t.append(e0.elapsed_time(e1))
+            td = tdist.max_over_ranks(statistics.median(t))
+            per_layer[L.name]["dense_us"] = round(td * 1e3, 2)
+            per_layer[L.name]["sfb_speedup_vs_dense"] = round(td / (per_layer[L.name]["sync_us"] / 1e3), 2)
+
+    # ---------------------------------------------------------------- e2e through host buffers
+    dWh = [torch.empty(l["L"].M, l["L"].N, dtype=tdt[cfg.out_dtype]).pin_memory() for l in layers]
+    h2d = sum(l["Xh"].numel() * l["Xh"].element_size() + l["dYh"].numel() * l["dYh"].element_size()
+              for l in layers)
+    d2h = sum(t.numel() * t.element_size() for t in dWh)
+    for _ in range(2):
+        with torch.cuda.stream(stream):
+            for l, h in zip(layers, dWh):
+                l["plan"].sync_host(l["Xh"], l["dYh"], h, stream)
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for _ in range(max(3, min(args.steps, 10))):
+        torch.cuda.synchronize()
+        tdist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        with torch.cuda.stream(stream):
+            for l, h in zip(layers, dWh):
+                l["plan"].sync_host(l["Xh"], l["dYh"], h, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    t_e2e = tdist.max_over_ranks(statistics.mean(e2e_ms))
+    e2e = {"value": round(n * dw_bytes / (t_e2e * 1e-3) / 1e9, 2), "unit": "GB/s",
+           "ms_per_step": round(t_e2e, 4), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "api": "tag_sfb_sync_host (pinned host X, dY in; full dW out)"}
+
+    clocks = clk.summary()
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu_baseline:
+        cpu = cpu_oracle_baseline(cfg, n)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t_step_ms, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": cfg.wire_dtype, "data": "synthetic", "config": config_json(cfg, n, args),
+                "per_layer": per_layer, "roofline": roofline, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
+                "lib": tag.version()}
+        print(json.dumps(line), flush=True)
+    for l in layers:
+        l["plan"].close()
+    comm.close()
+    if tdist.env_ranks()[2] > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

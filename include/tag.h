@@ -43,6 +43,9 @@
 #ifdef __cplusplus
 extern "C" {
 #endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* the library builds with -fvisibility=hidden */
+#endif
 
 typedef struct CUstream_st* tag_stream_t; /* == cudaStream_t; NULL = legacy default stream */
 
@@ -194,6 +197,9 @@ typedef struct {
 tag_status_t tag_sfb_select(const tag_layer_t* layers, int num_layers, const tag_topology_t* topo,
                             tag_choice_t* out);
 
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
 #ifdef __cplusplus
 }
 #endif

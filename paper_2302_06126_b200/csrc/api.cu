@@ -1,0 +1,486 @@
+// api.cu — the libtag C ABI (include/tag.h): communicator bootstrap, SFB plans, the SFB sync
+// path (pack -> NCCL all-gather -> tensor-core reconstruction) and the dense-AllReduce baseline.
+// Host-side orchestration only; every arithmetic step runs in the kernels of this library or in
+// NCCL. There is no CPU fallback.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "tag_internal.h"
+
+namespace tag {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local std::string t_last_error;
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+tag_status_t fail(tag_status_t st, const std::string& msg) {
+    t_last_error = msg;
+    return st;
+}
+tag_status_t cuda_fail(cudaError_t e, const char* what) {
+    t_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? TAG_ERR_OOM : TAG_ERR_CUDA;
+}
+static tag_status_t nccl_fail(ncclResult_t r, const char* what) {
+    t_last_error = std::string(what) + ": " + ncclGetErrorString(r);
+    return TAG_ERR_NCCL;
+}
+
+int num_sms() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cached[dev] == 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = 148;
+        cached[dev] = v;
+    }
+    return cached[dev];
+}
+
+// ------------------------------------------------------------------------------------------
+// scale kernel for the n = 1 "dense all-reduce" (dW <- dW / B) — no collective exists then
+// ------------------------------------------------------------------------------------------
+namespace {
+__global__ void scale_f32_kernel(float* p, int64_t len, float alpha) {
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = tid; i < len; i += nt) p[i] = __fmul_rn(p[i], alpha);
+}
+__global__ void scale_bf16_kernel(__nv_bfloat16* p, int64_t len, float alpha) {
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nt = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = tid; i < len; i += nt)
+        p[i] = __float2bfloat16_rn(__fmul_rn(__bfloat162float(p[i]), alpha));
+}
+}  // namespace
+
+}  // namespace tag
+
+using namespace tag;
+
+struct tag_comm_s {
+    ncclComm_t nccl = nullptr;   // nullptr when nranks == 1
+    int nranks = 1, rank = 0, device = 0;
+};
+
+struct tag_plan_s {
+    tag_comm_s* comm = nullptr;
+    tag_sfb_desc_t d{};
+    int64_t K = 0;
+    float alpha = 0.f;             // fl32(1/(nB))
+    bool use_tc = false;           // tensor-core reconstruction (else SIMT FFMA)
+    void* gx = nullptr;            // gathered X_all  (K x M, wire dtype)
+    void* gdy = nullptr;           // gathered dY_all (K x N, wire dtype)
+    const void* src_x = nullptr;   // operands of the next reconstruct (set by gather)
+    const void* src_dy = nullptr;
+    ncclRedOp_t premul{};
+    bool has_premul = false;
+    // device staging of tag_sfb_sync_host (allocated on first use)
+    void* st_x = nullptr;
+    void* st_dy = nullptr;
+    void* st_dw = nullptr;
+};
+
+namespace {
+
+ncclDataType_t nccl_type(tag_dtype_t t) { return t == TAG_F32 ? ncclFloat32 : ncclBfloat16; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+tag_status_t set_device(tag_comm_s* c) {
+    cudaError_t e = cudaSetDevice(c->device);
+    return e == cudaSuccess ? TAG_OK : cuda_fail(e, "cudaSetDevice");
+}
+
+tag_status_t check_async(tag_comm_s* c) {
+    if (!c->nccl) return TAG_OK;
+    ncclResult_t ar = ncclSuccess;
+    ncclResult_t r = ncclCommGetAsyncError(c->nccl, &ar);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclCommGetAsyncError");
+    if (ar != ncclSuccess && ar != ncclInProgress)
+        return fail(TAG_ERR_ASYNC, std::string("asynchronous NCCL error: ") + ncclGetErrorString(ar));
+    return TAG_OK;
+}
+
+#define TAG_TRY(expr)                         \
+    do {                                      \
+        tag_status_t _st = (expr);            \
+        if (_st != TAG_OK) return _st;        \
+    } while (0)
+
+tag_status_t validate_desc(const tag_comm_s* c, const tag_sfb_desc_t* d) {
+    if (d->M < 1 || d->N < 1 || d->B < 1)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: M, N, B must be >= 1");
+    if (d->n != c->nranks)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: desc.n must equal the comm size");
+    if (d->M > INT32_MAX || d->N > INT32_MAX || static_cast<int64_t>(d->n) * d->B > INT32_MAX)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: M, N and n*B must fit in int32");
+    auto okdt = [](tag_dtype_t t) { return t == TAG_F32 || t == TAG_BF16; };
+    if (!okdt(d->in_dtype) || !okdt(d->wire_dtype) || !okdt(d->out_dtype))
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: unknown dtype");
+    if (d->in_dtype == TAG_BF16 && d->wire_dtype == TAG_F32)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: bf16 -> fp32 wire is not a supported pair");
+    if (d->fuse_sgd != 0 && d->fuse_sgd != 1)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: fuse_sgd must be 0 or 1");
+    if (d->fuse_sgd && !(std::isfinite(d->lr) && std::isfinite(d->momentum) &&
+                         std::isfinite(d->weight_decay)))
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: non-finite SGD hyper-parameter");
+    return TAG_OK;
+}
+
+tag_status_t check_ptrs(const char* fn, std::initializer_list<const void*> ps) {
+    for (const void* p : ps) {
+        if (!p) return fail(TAG_ERR_INVALID_ARG, std::string(fn) + ": NULL pointer");
+        if (!aligned16(p)) return fail(TAG_ERR_INVALID_ARG, std::string(fn) + ": pointer not 16-byte aligned");
+    }
+    return TAG_OK;
+}
+
+bool needs_gather_buffers(const tag_sfb_desc_t& d) { return d.n > 1 || d.in_dtype != d.wire_dtype; }
+
+// a1 + a2: leaves the operands of the reconstruction in plan->src_x / src_dy
+tag_status_t do_gather(tag_plan_s* p, const void* X, const void* dY, cudaStream_t s) {
+    const tag_sfb_desc_t& d = p->d;
+    const int64_t cx = d.B * d.M, cy = d.B * d.N;          // elements per replica
+    const size_t ew = dtype_size(d.wire_dtype);
+    if (d.n == 1) {
+        if (d.in_dtype == d.wire_dtype) {
+            p->src_x = X;
+            p->src_dy = dY;
+            return TAG_OK;
+        }
+        TAG_TRY(launch_pack(X, p->gx, cx, dY, p->gdy, cy, d.in_dtype, d.wire_dtype, s));
+        p->src_x = p->gx;
+        p->src_dy = p->gdy;
+        return TAG_OK;
+    }
+    const int r = p->comm->rank;
+    char* gx = static_cast<char*>(p->gx);
+    char* gdy = static_cast<char*>(p->gdy);
+    const void* sx = X;
+    const void* sdy = dY;
+    if (d.in_dtype != d.wire_dtype) {
+        // a1: cast into this rank's slot, then gather in place
+        sx = gx + r * cx * ew;
+        sdy = gdy + r * cy * ew;
+        TAG_TRY(launch_pack(X, const_cast<void*>(sx), cx, dY, const_cast<void*>(sdy), cy,
+                            d.in_dtype, d.wire_dtype, s));
+    }
+    // a2: "broadcast to all devices" = all-gather of both factors, rank-major (R12).
+    // Same dtype: NCCL reads the caller's buffers directly (no pack pass over HBM).
+    const ncclDataType_t t = nccl_type(d.wire_dtype);
+    ncclResult_t nr = ncclGroupStart();
+    if (nr == ncclSuccess) nr = ncclAllGather(sx, gx, static_cast<size_t>(cx), t, p->comm->nccl, s);
+    if (nr == ncclSuccess) nr = ncclAllGather(sdy, gdy, static_cast<size_t>(cy), t, p->comm->nccl, s);
+    ncclResult_t ne = ncclGroupEnd();
+    if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather");
+    if (ne != ncclSuccess) return nccl_fail(ne, "ncclGroupEnd");
+    p->src_x = p->gx;
+    p->src_dy = p->gdy;
+    return TAG_OK;
+}
+
+tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int64_t K,
+                      float alpha, cudaStream_t s) {
+    if (!p->src_x) return fail(TAG_ERR_INVALID_ARG, "reconstruct: no factors gathered on this plan yet");
+    ReconArgs a{};
+    a.A = p->src_x;
+    a.Bm = p->src_dy;
+    a.C = dW;
+    a.M = p->d.M;
+    a.N = p->d.N;
+    a.K = K;
+    a.wire = p->d.wire_dtype;
+    a.out = p->d.out_dtype;
+    a.alpha = alpha;
+    a.sgd = sgd;
+    a.W = W;
+    a.V = V;
+    a.lr = p->d.lr;
+    a.mu = p->d.momentum;
+    a.wd = p->d.weight_decay;
+    if (p->use_tc && recon_tc_ok(a)) return launch_recon_tc(a, s);
+    return launch_recon_simt(a, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tag_version(void) { return "libtag 0.1.0 (sm_100a)"; }
+
+const char* tag_status_string(tag_status_t s) {
+    switch (s) {
+        case TAG_OK: return "TAG_OK";
+        case TAG_ERR_INVALID_ARG: return "TAG_ERR_INVALID_ARG";
+        case TAG_ERR_UNSUPPORTED: return "TAG_ERR_UNSUPPORTED";
+        case TAG_ERR_CUDA: return "TAG_ERR_CUDA";
+        case TAG_ERR_NCCL: return "TAG_ERR_NCCL";
+        case TAG_ERR_OOM: return "TAG_ERR_OOM";
+        case TAG_ERR_NOT_INITIALIZED: return "TAG_ERR_NOT_INITIALIZED";
+        case TAG_ERR_ASYNC: return "TAG_ERR_ASYNC";
+    }
+    return "TAG_ERR_UNKNOWN";
+}
+
+const char* tag_last_error(void) { return t_last_error.c_str(); }
+
+uint64_t tag_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+tag_status_t tag_get_unique_id(unsigned char id[128]) {
+    if (!id) return fail(TAG_ERR_INVALID_ARG, "tag_get_unique_id: NULL id");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId u;
+    ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclGetUniqueId");
+    std::memcpy(id, &u, 128);
+    return TAG_OK;
+}
+
+tag_status_t tag_comm_create(const unsigned char id[128], int nranks, int rank, int cuda_device,
+                             tag_comm_t* out) {
+    if (!out) return fail(TAG_ERR_INVALID_ARG, "tag_comm_create: NULL out");
+    if (nranks < 1 || rank < 0 || rank >= nranks || cuda_device < 0)
+        return fail(TAG_ERR_INVALID_ARG, "tag_comm_create: bad nranks/rank/device");
+    if (nranks > 1 && !id) return fail(TAG_ERR_INVALID_ARG, "tag_comm_create: NULL id");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (cuda_device >= ndev) return fail(TAG_ERR_INVALID_ARG, "tag_comm_create: no such CUDA device");
+    e = cudaSetDevice(cuda_device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    tag_comm_s* c = new tag_comm_s;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = cuda_device;
+    if (nranks > 1) {
+        ncclUniqueId u;
+        std::memcpy(&u, id, 128);
+        ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+        if (r != ncclSuccess) {
+            delete c;
+            return nccl_fail(r, "ncclCommInitRank");
+        }
+    }
+    *out = c;
+    return TAG_OK;
+}
+
+tag_status_t tag_comm_destroy(tag_comm_t c) {
+    if (!c) return TAG_OK;
+    tag_status_t st = TAG_OK;
+    if (c->nccl) {
+        ncclResult_t r = ncclCommDestroy(c->nccl);
+        if (r != ncclSuccess) st = nccl_fail(r, "ncclCommDestroy");
+    }
+    delete c;
+    return st;
+}
+
+tag_status_t tag_comm_info(tag_comm_t c, int* nranks, int* rank, int* cuda_device) {
+    if (!c) return fail(TAG_ERR_INVALID_ARG, "tag_comm_info: NULL comm");
+    if (nranks) *nranks = c->nranks;
+    if (rank) *rank = c->rank;
+    if (cuda_device) *cuda_device = c->device;
+    return TAG_OK;
+}
+
+tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t* out) {
+    if (!c || !d || !out) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: NULL argument");
+    TAG_TRY(validate_desc(c, d));
+    TAG_TRY(set_device(c));
+    tag_plan_s* p = new tag_plan_s;
+    p->comm = c;
+    p->d = *d;
+    p->K = static_cast<int64_t>(d->n) * d->B;
+    p->alpha = static_cast<float>(1.0 / static_cast<double>(p->K));   // fl32(1/(nB)), R1
+    // tensor cores need 16-byte factor rows and bf16 operands (fp32 wire: SIMT FFMA, R10)
+    p->use_tc = d->wire_dtype == TAG_BF16 && d->M % 8 == 0 && d->N % 8 == 0;
+    auto cleanup = [p]() {
+        cudaFree(p->gx);
+        cudaFree(p->gdy);
+        delete p;
+    };
+    if (needs_gather_buffers(*d)) {
+        const size_t ew = dtype_size(d->wire_dtype);
+        cudaError_t e = cudaMalloc(&p->gx, static_cast<size_t>(p->K * d->M) * ew);
+        if (e == cudaSuccess) e = cudaMalloc(&p->gdy, static_cast<size_t>(p->K * d->N) * ew);
+        if (e != cudaSuccess) {
+            cleanup();
+            return cuda_fail(e, "tag_sfb_plan: cudaMalloc(gather buffers)");
+        }
+    }
+    if (c->nccl) {
+        // dense baseline: the 1/(nB) scale rides inside the AllReduce (PreMulSum)
+        ncclResult_t r;
+        if (d->out_dtype == TAG_F32) {
+            float a = p->alpha;
+            r = ncclRedOpCreatePreMulSum(&p->premul, &a, ncclFloat32, ncclScalarHostImmediate, c->nccl);
+        } else {
+            __nv_bfloat16 a = __float2bfloat16_rn(p->alpha);
+            r = ncclRedOpCreatePreMulSum(&p->premul, &a, ncclBfloat16, ncclScalarHostImmediate, c->nccl);
+        }
+        if (r != ncclSuccess) {
+            cleanup();
+            return nccl_fail(r, "ncclRedOpCreatePreMulSum");
+        }
+        p->has_premul = true;
+    }
+    *out = p;
+    return TAG_OK;
+}
+
+tag_status_t tag_sfb_plan_destroy(tag_sfb_plan_t p) {
+    if (!p) return TAG_OK;
+    set_device(p->comm);
+    if (p->has_premul) ncclRedOpDestroy(p->premul, p->comm->nccl);
+    cudaFree(p->gx);
+    cudaFree(p->gdy);
+    cudaFree(p->st_x);
+    cudaFree(p->st_dy);
+    cudaFree(p->st_dw);
+    delete p;
+    return TAG_OK;
+}
+
+tag_status_t tag_sfb_gather(tag_sfb_plan_t p, const void* X, const void* dY, tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_gather: NULL plan");
+    TAG_TRY(check_ptrs("tag_sfb_gather", {X, dY}));
+    TAG_TRY(set_device(p->comm));
+    TAG_TRY(check_async(p->comm));
+    return do_gather(p, X, dY, reinterpret_cast<cudaStream_t>(stream));
+}
+
+tag_status_t tag_sfb_reconstruct(tag_sfb_plan_t p, void* dW_out, tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_reconstruct: NULL plan");
+    TAG_TRY(check_ptrs("tag_sfb_reconstruct", {dW_out}));
+    TAG_TRY(set_device(p->comm));
+    return do_recon(p, dW_out, false, nullptr, nullptr, p->K, p->alpha,
+                    reinterpret_cast<cudaStream_t>(stream));
+}
+
+tag_status_t tag_sfb_sync(tag_sfb_plan_t p, const void* X, const void* dY, void* dW_out,
+                          tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync: NULL plan");
+    TAG_TRY(check_ptrs("tag_sfb_sync", {X, dY, dW_out}));
+    TAG_TRY(set_device(p->comm));
+    TAG_TRY(check_async(p->comm));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    TAG_TRY(do_gather(p, X, dY, s));
+    return do_recon(p, dW_out, false, nullptr, nullptr, p->K, p->alpha, s);
+}
+
+tag_status_t tag_sfb_sync_sgd(tag_sfb_plan_t p, const void* X, const void* dY, float* W, float* v,
+                              void* dW_out, tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sgd: NULL plan");
+    if (!p->d.fuse_sgd) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sgd: plan has fuse_sgd = 0");
+    TAG_TRY(check_ptrs("tag_sfb_sync_sgd", {X, dY, W, v}));
+    if (dW_out) TAG_TRY(check_ptrs("tag_sfb_sync_sgd", {dW_out}));
+    TAG_TRY(set_device(p->comm));
+    TAG_TRY(check_async(p->comm));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    TAG_TRY(do_gather(p, X, dY, s));
+    return do_recon(p, dW_out, true, W, v, p->K, p->alpha, s);
+}
+
+tag_status_t tag_sfb_sync_host(tag_sfb_plan_t p, const void* X_host, const void* dY_host,
+                               void* dW_host, tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_host: NULL plan");
+    if (!X_host || !dY_host || !dW_host) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_host: NULL pointer");
+    TAG_TRY(set_device(p->comm));
+    TAG_TRY(check_async(p->comm));
+    const tag_sfb_desc_t& d = p->d;
+    const size_t bx = static_cast<size_t>(d.B * d.M) * dtype_size(d.in_dtype);
+    const size_t bdy = static_cast<size_t>(d.B * d.N) * dtype_size(d.in_dtype);
+    const size_t bdw = static_cast<size_t>(d.M * d.N) * dtype_size(d.out_dtype);
+    if (!p->st_x) {
+        cudaError_t e = cudaMalloc(&p->st_x, bx);
+        if (e == cudaSuccess) e = cudaMalloc(&p->st_dy, bdy);
+        if (e == cudaSuccess) e = cudaMalloc(&p->st_dw, bdw);
+        if (e != cudaSuccess) {
+            cudaFree(p->st_x);
+            cudaFree(p->st_dy);
+            cudaFree(p->st_dw);
+            p->st_x = p->st_dy = p->st_dw = nullptr;
+            return cuda_fail(e, "tag_sfb_sync_host: cudaMalloc(staging)");
+        }
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemcpyAsync(p->st_x, X_host, bx, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(p->st_dy, dY_host, bdy, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "tag_sfb_sync_host: H2D copy");
+    TAG_TRY(do_gather(p, p->st_x, p->st_dy, s));
+    TAG_TRY(do_recon(p, p->st_dw, false, nullptr, nullptr, p->K, p->alpha, s));
+    e = cudaMemcpyAsync(dW_host, p->st_dw, bdw, cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "tag_sfb_sync_host: D2H copy");
+    return TAG_OK;
+}
+
+tag_status_t tag_local_grad(tag_sfb_plan_t p, const void* X, const void* dY, void* dW_local,
+                            tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_local_grad: NULL plan");
+    TAG_TRY(check_ptrs("tag_local_grad", {X, dY, dW_local}));
+    TAG_TRY(set_device(p->comm));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const tag_sfb_desc_t& d = p->d;
+    if (d.in_dtype != d.wire_dtype) {
+        // same operand precision as the SFB path: cast into this rank's gather slot first
+        const size_t ew = dtype_size(d.wire_dtype);
+        const int r = p->comm->rank;
+        void* lx = static_cast<char*>(p->gx) + r * d.B * d.M * ew;
+        void* ldy = static_cast<char*>(p->gdy) + r * d.B * d.N * ew;
+        TAG_TRY(launch_pack(X, lx, d.B * d.M, dY, ldy, d.B * d.N, d.in_dtype, d.wire_dtype, s));
+        p->src_x = lx;
+        p->src_dy = ldy;
+    } else {
+        p->src_x = X;
+        p->src_dy = dY;
+    }
+    tag_status_t st = do_recon(p, dW_local, false, nullptr, nullptr, d.B, 1.0f, s);
+    p->src_x = p->src_dy = nullptr;   // a later reconstruct needs a fresh gather
+    return st;
+}
+
+tag_status_t tag_dense_allreduce(tag_sfb_plan_t p, void* dW, tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_dense_allreduce: NULL plan");
+    TAG_TRY(check_ptrs("tag_dense_allreduce", {dW}));
+    TAG_TRY(set_device(p->comm));
+    TAG_TRY(check_async(p->comm));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t len = p->d.M * p->d.N;
+    if (!p->comm->nccl) {
+        const int grid = num_sms() * 4;
+        if (p->d.out_dtype == TAG_F32)
+            scale_f32_kernel<<<grid, 256, 0, s>>>(static_cast<float*>(dW), len, p->alpha);
+        else
+            scale_bf16_kernel<<<grid, 256, 0, s>>>(static_cast<__nv_bfloat16*>(dW), len, p->alpha);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "launch scale kernel");
+        count_launch();
+        return TAG_OK;
+    }
+    ncclResult_t r = ncclAllReduce(dW, dW, static_cast<size_t>(len), nccl_type(p->d.out_dtype),
+                                   p->premul, p->comm->nccl, s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclAllReduce");
+    return TAG_OK;
+}
+
+tag_status_t tag_sgd_step(tag_sfb_plan_t p, const float* dW, float* W, float* v,
+                          tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sgd_step: NULL plan");
+    TAG_TRY(check_ptrs("tag_sgd_step", {dW, W, v}));
+    TAG_TRY(set_device(p->comm));
+    return launch_sgd(dW, W, v, p->d.M * p->d.N, p->d.lr, p->d.momentum, p->d.weight_decay,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

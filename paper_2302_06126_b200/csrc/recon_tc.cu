@@ -1,0 +1,394 @@
+// recon_tc.cu — step a3+a4 of the SFB path on the 5th-generation tensor cores.
+//
+// dW = alpha * X_all^T dY_all ("MatMul ops on each device can reconstruct identical
+// gradients"), K = n*B gathered factor rows, alpha = 1/(nB) (DESIGN R1), fused epilogue
+// (E1: scale + fp32/bf16 store; E2: scale + SGD-momentum on W, v, P:543-545 / R14).
+//
+// Operand layout: both factors are MN-major in their natural row-major form — A_mma[m][k] =
+// X_all[k][m] with m contiguous, B_mma[j][k] = dY_all[k][j] with j contiguous — so no transpose
+// pass exists anywhere on the path. TMA loads 64-element (128-byte) MN chunks x BK rows with the
+// 128-byte swizzle; the UMMA descriptors describe the canonical MN-major SW128 layout
+// (LBO = stride between MN chunks, SBO = 1024 B between 8-row K groups).
+//
+// Kernel structure (persistent, warp-specialised, one CTA per SM):
+//   warp 0      TMA producer: STAGES-deep smem ring of {A: 128 x BK, B: BN x BK} tiles
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer; accumulators double-buffered
+//               in TMEM (2 x BN fp32 columns) so tile t+1's MMAs overlap tile t's epilogue
+//   warps 2..9  epilogue: tcgen05.ld 32 rows x 32 cols -> scale -> swizzled smem -> TMA store
+//               (E1), or the fused SGD update on W, v (E2). Each TMEM lane quadrant is drained by
+//               two warps, each owning half of the tile's columns.
+// At the paper's small-batch shapes (K = 32..2048) the epilogue's HBM write of the M x N
+// gradient is the binding roof (DESIGN "Roofline"), so the kernel keeps 8 warps of stores in
+// flight while the tensor core works one tile ahead.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "ptx.cuh"
+#include "tag_internal.h"
+
+namespace tag {
+namespace {
+
+constexpr int BM = 128;                  // UMMA M (TMEM lanes)
+constexpr int BK = 32;                   // factor rows per pipeline stage
+constexpr int NUM_EPI_WARPS = 8;
+constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;   // 320
+constexpr int CHUNK_BYTES = BK * 128;    // one 128-byte-wide MN chunk of BK rows (4 KB)
+constexpr int EPI_BUF_BYTES = 32 * 128;  // 32 rows x 128 B staging for one TMA store
+constexpr int TMEM_COLS = 512;
+
+template <int BN>
+struct Cfg {
+    static constexpr int A_BYTES = (BM / 64) * CHUNK_BYTES;
+    static constexpr int B_BYTES = (BN / 64) * CHUNK_BYTES;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = BN == 256 ? 6 : 8;
+    static constexpr int EPI_BYTES = NUM_EPI_WARPS * 2 * EPI_BUF_BYTES;
+    static constexpr int BAR_BYTES = 256;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
+    // kind::f16 instruction descriptor: D f32, A/B bf16, both MN-major, N = BN, M = 128.
+    static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+                                      (1u << 16) | (uint32_t(BN >> 3) << 17) |
+                                      (uint32_t(BM >> 4) << 24);
+};
+
+struct Params {
+    int M, N, K;
+    int num_n_blocks, num_tiles, num_k_blocks;
+    float alpha;
+    float* W;
+    float* V;
+    float lr, mu, wd;
+    int write_dw;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);   // RNE, lo in the low half
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int BN, bool OUT_BF16, bool SGD>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmC, const Params p)
+{
+    using C = Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    // 1024-byte alignment for the SWIZZLE_128B atoms
+    const uint32_t base = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
+    const uint32_t s_stages = base;
+    const uint32_t s_epi = s_stages + C::STAGES * C::STAGE_BYTES;
+    const uint32_t s_bar = s_epi + C::EPI_BYTES;
+    const uint32_t bar_full = s_bar;                       // [STAGES]
+    const uint32_t bar_empty = s_bar + 8 * C::STAGES;      // [STAGES]
+    const uint32_t bar_tfull = s_bar + 16 * C::STAGES;     // [2]
+    const uint32_t bar_tempty = bar_tfull + 16;            // [2]
+    const uint32_t s_tmem_slot = bar_tempty + 16;
+    uint8_t* gen_base = smem_raw + (base - ptx::smem_addr(smem_raw));
+    volatile uint32_t* tmem_slot_ptr =
+        reinterpret_cast<volatile uint32_t*>(gen_base + (s_tmem_slot - base));
+
+    const uint32_t warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+        if (!SGD || p.write_dw) ptx::tma_prefetch_desc(&tmC);
+        for (int s = 0; s < C::STAGES; ++s) {
+            ptx::mbar_init(bar_full + 8 * s, 1);
+            ptx::mbar_init(bar_empty + 8 * s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(bar_tfull + 8 * a, 1);
+            ptx::mbar_init(bar_tempty + 8 * a, NUM_EPI_WARPS);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(s_tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot_ptr;
+
+    if (warp == 0) {
+        // ===================================================== TMA producer
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                const int m0 = (tile / p.num_n_blocks) * BM;
+                const int n0 = (tile % p.num_n_blocks) * BN;
+                for (int kb = 0; kb < p.num_k_blocks; ++kb) {
+                    ptx::mbar_wait(bar_empty + 8 * stage, phase ^ 1);
+                    const uint32_t fb = bar_full + 8 * stage;
+                    ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+                    const uint32_t sa = s_stages + stage * C::STAGE_BYTES;
+                    const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+                    for (int c = 0; c < BM / 64; ++c)
+                        ptx::tma_load_2d(sa + c * CHUNK_BYTES, &tmA, fb, m0 + 64 * c, kb * BK);
+#pragma unroll
+                    for (int c = 0; c < BN / 64; ++c)
+                        ptx::tma_load_2d(sb + c * CHUNK_BYTES, &tmB, fb, n0 + 64 * c, kb * BK);
+                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================================================== MMA issuer (one thread)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+                ptx::mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);   // epilogue drained it
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < p.num_k_blocks; ++kb) {
+                    ptx::mbar_wait(bar_full + 8 * stage, phase);        // TMA landed
+                    ptx::tc_fence_after();
+                    const uint32_t sa = s_stages + stage * C::STAGE_BYTES;
+                    const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        // 16 K rows = two 8-row swizzle atoms = 2048 bytes per UMMA_K step
+                        const uint64_t ad = ptx::sw128_desc(sa + kk * 2048, CHUNK_BYTES, 1024);
+                        const uint64_t bd = ptx::sw128_desc(sb + kk * 2048, CHUNK_BYTES, 1024);
+                        ptx::mma_f16(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0);
+                    }
+                    ptx::mma_commit(bar_empty + 8 * stage);            // frees the smem slot
+                    if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit(bar_tfull + 8 * acc);                   // accumulator ready
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ===================================================== epilogue warps
+        const int ew = warp - 2;                 // 0..7
+        const int quad = warp & 3;               // TMEM lane quadrant this warp may access
+        const int half = ew >> 2;                // which half of the tile's columns
+        const uint32_t my_buf = s_epi + ew * 2 * EPI_BUF_BYTES;
+        int buf = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        constexpr int COLS_PER_CHUNK = OUT_BF16 ? 64 : 32;    // 128 bytes of output per row
+        constexpr int CHUNKS = (BN / 2) / COLS_PER_CHUNK;
+        const float alpha = p.alpha;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            const int m0 = (tile / p.num_n_blocks) * BM;
+            const int n0 = (tile % p.num_n_blocks) * BN;
+            const int row0 = m0 + 32 * quad;     // first output row of this warp
+            ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
+            ptx::tc_fence_after();
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quad) << 16) + acc * BN;
+#pragma unroll 1
+            for (int ch = 0; ch < CHUNKS; ++ch) {
+                const int col = half * (BN / 2) + ch * COLS_PER_CHUNK;   // within the tile
+                if (n0 + col >= p.N) break;                              // warp-uniform
+                uint32_t w[32];                                          // 128 B of this row
+                if constexpr (OUT_BF16) {
+                    uint32_t r0[32], r1[32];
+                    ptx::tmem_ld_32x32b_x32(t_row + col, r0);
+                    ptx::tmem_ld_32x32b_x32(t_row + col + 32, r1);
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        w[i] = pack_bf16x2(__fmul_rn(__uint_as_float(r0[2 * i]), alpha),
+                                           __fmul_rn(__uint_as_float(r0[2 * i + 1]), alpha));
+                        w[16 + i] = pack_bf16x2(__fmul_rn(__uint_as_float(r1[2 * i]), alpha),
+                                                __fmul_rn(__uint_as_float(r1[2 * i + 1]), alpha));
+                    }
+                } else {
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(t_row + col, r);
+                    ptx::tmem_wait_ld();
+                    if constexpr (SGD) {
+                        // E2: g = alpha*acc + wd*W ; v = mu*v + g ; W -= lr*v   (fp32, R14)
+                        const int grow = row0 + static_cast<int>(lane);
+                        const int gcol = n0 + col;
+                        if (grow < p.M) {
+                            float* wp = p.W + static_cast<int64_t>(grow) * p.N + gcol;
+                            float* vp = p.V + static_cast<int64_t>(grow) * p.N + gcol;
+                            const int nvalid = min(32, p.N - gcol);
+                            if (nvalid == 32) {
+                                float4 wv[8], vv[8];
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) {
+                                    wv[i] = reinterpret_cast<const float4*>(wp)[i];
+                                    vv[i] = reinterpret_cast<const float4*>(vp)[i];
+                                }
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) {
+                                    float* wf = reinterpret_cast<float*>(&wv[i]);
+                                    float* vf = reinterpret_cast<float*>(&vv[i]);
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e) {
+                                        const float d = __fmul_rn(__uint_as_float(r[4 * i + e]), alpha);
+                                        const float g = __fadd_rn(d, __fmul_rn(p.wd, wf[e]));
+                                        vf[e] = __fadd_rn(__fmul_rn(p.mu, vf[e]), g);
+                                        wf[e] = __fsub_rn(wf[e], __fmul_rn(p.lr, vf[e]));
+                                    }
+                                }
+#pragma unroll
+                                for (int i = 0; i < 8; ++i) {
+                                    reinterpret_cast<float4*>(wp)[i] = wv[i];
+                                    reinterpret_cast<float4*>(vp)[i] = vv[i];
+                                }
+                            } else {
+                                for (int e = 0; e < nvalid; ++e) {
+                                    const float d = __fmul_rn(__uint_as_float(r[e]), alpha);
+                                    const float g = __fadd_rn(d, __fmul_rn(p.wd, wp[e]));
+                                    const float vn = __fadd_rn(__fmul_rn(p.mu, vp[e]), g);
+                                    vp[e] = vn;
+                                    wp[e] = __fsub_rn(wp[e], __fmul_rn(p.lr, vn));
+                                }
+                            }
+                        }
+                        if (!p.write_dw) continue;
+                    }
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        w[i] = __float_as_uint(__fmul_rn(__uint_as_float(r[i]), alpha));
+                }
+                // staging buffer free? (its previous TMA store has finished reading smem)
+                if (lane == 0) ptx::bulk_wait_read<1>();
+                __syncwarp();
+                const uint32_t sbuf = my_buf + buf * EPI_BUF_BYTES;
+                const uint32_t rowaddr = sbuf + lane * 128;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)   // 16-byte chunk j of this row, 128B-swizzled
+                    ptx::st_shared_v4(rowaddr + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1],
+                                      w[4 * j + 2], w[4 * j + 3]);
+                ptx::fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::tma_store_2d(&tmC, sbuf, n0 + col, row0);
+                    ptx::bulk_commit();
+                }
+                buf ^= 1;
+            }
+            // all TMEM reads of this accumulator are complete (wait::ld above)
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+        if (lane == 0) ptx::bulk_wait<0>();
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+                cudaSuccess && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+// Row-major rows x cols matrix; box = box_cols x box_rows; 128-byte swizzle.
+bool encode_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esize, int64_t rows,
+               int64_t cols, int box_cols, int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols * esize)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool OUT_BF16, bool SGD>
+tag_status_t launch_t(const ReconArgs& a, cudaStream_t s) {
+    using C = Cfg<BN>;
+    CUtensorMap tmA, tmB, tmC;
+    if (!encode_2d(&tmA, a.A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.K, a.M, 64, BK) ||
+        !encode_2d(&tmB, a.Bm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.K, a.N, 64, BK))
+        return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
+    const bool write_dw = a.C != nullptr;
+    if (write_dw) {
+        const bool ok = OUT_BF16
+            ? encode_2d(&tmC, a.C, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.M, a.N, 64, 32)
+            : encode_2d(&tmC, a.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.M, a.N, 32, 32);
+        if (!ok) return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for dW");
+    } else {
+        tmC = tmA;  // unused
+    }
+    Params p;
+    p.M = static_cast<int>(a.M);
+    p.N = static_cast<int>(a.N);
+    p.K = static_cast<int>(a.K);
+    p.num_n_blocks = static_cast<int>((a.N + BN - 1) / BN);
+    const int num_m_blocks = static_cast<int>((a.M + BM - 1) / BM);
+    p.num_tiles = num_m_blocks * p.num_n_blocks;
+    p.num_k_blocks = static_cast<int>((a.K + BK - 1) / BK);
+    p.alpha = a.alpha;
+    p.W = a.W;
+    p.V = a.V;
+    p.lr = a.lr;
+    p.mu = a.mu;
+    p.wd = a.wd;
+    p.write_dw = write_dw ? 1 : 0;
+    auto kern = recon_tc_kernel<BN, OUT_BF16, SGD>;
+    static bool attr_set = false;   // per instantiation
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::SMEM);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recon_tc)");
+        attr_set = true;
+    }
+    const int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
+    kern<<<grid, NUM_THREADS, C::SMEM, s>>>(tmA, tmB, tmC, p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "launch recon_tc_kernel");
+    count_launch();
+    return TAG_OK;
+}
+
+}  // namespace
+
+bool recon_tc_ok(const ReconArgs& a) {
+    if (a.wire != TAG_BF16) return false;                 // tf32 path: later
+    if (a.M % 8 || a.N % 8) return false;                 // 16-byte rows for TMA (bf16)
+    if (a.M > INT32_MAX || a.N > INT32_MAX || a.K > INT32_MAX) return false;
+    if (a.sgd && a.out == TAG_BF16 && a.C) return false;  // E2 writes fp32 dW only
+    if (reinterpret_cast<uintptr_t>(a.A) % 16 || reinterpret_cast<uintptr_t>(a.Bm) % 16)
+        return false;
+    if (a.C && reinterpret_cast<uintptr_t>(a.C) % 16) return false;
+    if (a.sgd && (reinterpret_cast<uintptr_t>(a.W) % 16 || reinterpret_cast<uintptr_t>(a.V) % 16))
+        return false;
+    return true;
+}
+
+tag_status_t launch_recon_tc(const ReconArgs& a, cudaStream_t s) {
+    // BN = 256 when there are enough tiles to fill every SM at least twice; else BN = 128.
+    const int64_t tiles256 = ((a.M + BM - 1) / BM) * ((a.N + 255) / 256);
+    const bool wide = tiles256 >= 2 * num_sms();
+    if (a.sgd) return wide ? launch_t<256, false, true>(a, s) : launch_t<128, false, true>(a, s);
+    if (a.out == TAG_BF16)
+        return wide ? launch_t<256, true, false>(a, s) : launch_t<128, true, false>(a, s);
+    return wide ? launch_t<256, false, false>(a, s) : launch_t<128, false, false>(a, s);
+}
+
+}  // namespace tag

@@ -1,0 +1,59 @@
+// tag_internal.h — declarations shared by the libtag translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <atomic>
+#include <cstdint>
+#include <string>
+
+#include "../../include/tag.h"
+
+namespace tag {
+
+// Thread-local error detail behind tag_last_error().
+void set_error(const std::string& msg);
+tag_status_t fail(tag_status_t st, const std::string& msg);
+tag_status_t cuda_fail(cudaError_t e, const char* what);
+
+// Kernel-launch counter behind tag_kernel_launches().
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t k = 1) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+int num_sms();
+
+inline size_t dtype_size(tag_dtype_t t) { return t == TAG_F32 ? 4 : 2; }
+
+// ------------------------------------------------------------------ reconstruction kernels
+// dW[m][j] = alpha * sum_{k<K} A[k][m] * Bm[k][j] (A: K x M, Bm: K x N, row-major, wire dtype),
+// written as out dtype (epilogue E1), or with the fused SGD-momentum update (epilogue E2).
+struct ReconArgs {
+    const void* A;       // K x M
+    const void* Bm;      // K x N
+    void* C;             // M x N, out dtype; may be nullptr when sgd (no dW write)
+    int64_t M, N, K;
+    tag_dtype_t wire;    // operand dtype
+    tag_dtype_t out;     // C dtype
+    float alpha;
+    // E2
+    bool sgd;
+    float* W;
+    float* V;
+    float lr, mu, wd;
+};
+
+// Tensor-core path (tcgen05 + TMEM + TMA). Requires 16-byte aligned rows (see recon_tc_ok).
+bool recon_tc_ok(const ReconArgs& a);
+tag_status_t launch_recon_tc(const ReconArgs& a, cudaStream_t s);
+// SIMT FFMA path: any shape, fp32 or bf16 operands (exact fp32 accumulation in k order).
+tag_status_t launch_recon_simt(const ReconArgs& a, cudaStream_t s);
+
+// ------------------------------------------------------------------ pack (a1)
+// Casts src (fp32) into dst (bf16, RNE) for two segments in one launch; or copies when the
+// dtypes match. Counts are elements.
+tag_status_t launch_pack(const void* x, void* x_dst, int64_t nx, const void* dy, void* dy_dst,
+                         int64_t ny, tag_dtype_t in, tag_dtype_t wire, cudaStream_t s);
+
+// ------------------------------------------------------------------ unfused SGD
+tag_status_t launch_sgd(const float* dW, float* W, float* V, int64_t len, float lr, float mu,
+                        float wd, cudaStream_t s);
+
+}  // namespace tag

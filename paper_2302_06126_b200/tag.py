@@ -1,0 +1,249 @@
+"""ctypes binding of libtag.so — the C ABI declared in include/tag.h.
+
+Argument marshalling only: tensors are checked (device, dtype, shape, contiguity) and their data
+pointers handed to the library; every step of the SFB path runs in libtag's CUDA kernels or in
+NCCL. There is no fallback: if libtag.so is missing, importing this module raises; if CUDA is
+unavailable, every compute call raises TagError.
+"""
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtag.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libtag.so not built ({LIB_PATH}); run __graft_entry__.build() or "
+                      f"`make -C {os.path.join(_HERE, 'csrc')}`")
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ------------------------------------------------------------------ enums (tag.h)
+OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_NOT_INITIALIZED, ERR_ASYNC = \
+    range(8)
+F32, BF16 = 0, 1
+SYNC_ALLREDUCE, SYNC_SFB, SYNC_NONE = 0, 1, 2
+RULE_NORTHSTAR, RULE_PAPER_ILP, RULE_WIRE = 0, 1, 2
+
+_TORCH_DT = {F32: torch.float32, BF16: torch.bfloat16}
+_DT_OF = {torch.float32: F32, torch.bfloat16: BF16, "f32": F32, "bf16": BF16, F32: F32, BF16: BF16}
+
+
+class SfbDesc(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int64), ("N", ctypes.c_int64), ("B", ctypes.c_int64),
+                ("n", ctypes.c_int), ("in_dtype", ctypes.c_int), ("wire_dtype", ctypes.c_int),
+                ("out_dtype", ctypes.c_int), ("fuse_sgd", ctypes.c_int), ("lr", ctypes.c_float),
+                ("momentum", ctypes.c_float), ("weight_decay", ctypes.c_float)]
+
+
+class LayerDesc(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int64), ("N", ctypes.c_int64), ("B", ctypes.c_int64),
+                ("factor_dtype", ctypes.c_int), ("grad_dtype", ctypes.c_int)]
+
+
+class Topology(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("link_bytes_per_s", ctypes.c_uint64),
+                ("tensor_flops", ctypes.c_uint64), ("rule", ctypes.c_int)]
+
+
+_p, _vp, _i, _st = ctypes.POINTER, ctypes.c_void_p, ctypes.c_int, ctypes.c_int
+_SIGS = {
+    "tag_version": ([], ctypes.c_char_p),
+    "tag_status_string": ([_i], ctypes.c_char_p),
+    "tag_last_error": ([], ctypes.c_char_p),
+    "tag_kernel_launches": ([], ctypes.c_uint64),
+    "tag_get_unique_id": ([ctypes.c_char_p], _st),
+    "tag_comm_create": ([ctypes.c_char_p, _i, _i, _i, _p(_vp)], _st),
+    "tag_comm_destroy": ([_vp], _st),
+    "tag_comm_info": ([_vp, _p(_i), _p(_i), _p(_i)], _st),
+    "tag_sfb_plan": ([_vp, _p(SfbDesc), _p(_vp)], _st),
+    "tag_sfb_plan_destroy": ([_vp], _st),
+    "tag_sfb_sync": ([_vp, _vp, _vp, _vp, _vp], _st),
+    "tag_sfb_gather": ([_vp, _vp, _vp, _vp], _st),
+    "tag_sfb_reconstruct": ([_vp, _vp, _vp], _st),
+    "tag_sfb_sync_sgd": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], _st),
+    "tag_sfb_sync_host": ([_vp, _vp, _vp, _vp, _vp], _st),
+    "tag_local_grad": ([_vp, _vp, _vp, _vp, _vp], _st),
+    "tag_dense_allreduce": ([_vp, _vp, _vp], _st),
+    "tag_sgd_step": ([_vp, _vp, _vp, _vp, _vp], _st),
+    "tag_sfb_select": ([_p(LayerDesc), _i, _p(Topology), _p(_i)], _st),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = _res
+EXPORTS = tuple(_SIGS)
+
+
+class TagError(RuntimeError):
+    def __init__(self, status, where):
+        self.status = status
+        detail = _lib.tag_last_error().decode(errors="replace")
+        name = _lib.tag_status_string(status).decode()
+        super().__init__(f"{where}: {name}: {detail}")
+
+
+def _check(st, where):
+    if st != OK:
+        raise TagError(st, where)
+
+
+def version():
+    return _lib.tag_version().decode()
+
+
+def kernel_launches():
+    """libtag kernels launched by this process so far."""
+    return int(_lib.tag_kernel_launches())
+
+
+def _stream(stream):
+    if stream is None:
+        return _vp(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return _vp(stream)
+    return _vp(stream.cuda_stream)
+
+
+def _dev(t, dtype, shape, name):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return _vp(t.data_ptr())
+
+
+def _host(t, dtype, shape, name):
+    if not isinstance(t, torch.Tensor) or t.is_cuda:
+        raise TypeError(f"{name} must be a host (CPU) tensor")
+    if t.dtype != dtype or tuple(t.shape) != tuple(shape) or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous {dtype} tensor of shape {tuple(shape)}")
+    return _vp(t.data_ptr())
+
+
+def unique_id():
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.tag_get_unique_id(buf), "tag_get_unique_id")
+    return buf.raw
+
+
+class Comm:
+    """One process per GPU. nranks == 1 needs no id (no NCCL communicator is created)."""
+
+    def __init__(self, nranks, rank, device, uid=None):
+        h = _vp()
+        idbuf = ctypes.create_string_buffer(uid, 128) if uid is not None else None
+        _check(_lib.tag_comm_create(idbuf, nranks, rank, device, ctypes.byref(h)),
+               "tag_comm_create")
+        self._h = h
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            _check(_lib.tag_comm_destroy(self._h), "tag_comm_destroy")
+            self._h = None
+
+
+class SfbPlan:
+    """One replicated Dense layer W (M x N), B rows per replica, n replicas (= comm size)."""
+
+    def __init__(self, comm, M, N, B, in_dtype="bf16", wire_dtype="bf16", out_dtype="f32",
+                 fuse_sgd=False, lr=0.0, momentum=0.0, weight_decay=0.0):
+        self.comm = comm
+        self.M, self.N, self.B, self.n = M, N, B, comm.nranks
+        self.in_dtype, self.wire_dtype, self.out_dtype = (_DT_OF[in_dtype], _DT_OF[wire_dtype],
+                                                          _DT_OF[out_dtype])
+        d = SfbDesc(M, N, B, comm.nranks, self.in_dtype, self.wire_dtype, self.out_dtype,
+                    1 if fuse_sgd else 0, lr, momentum, weight_decay)
+        h = _vp()
+        _check(_lib.tag_sfb_plan(comm.handle, ctypes.byref(d), ctypes.byref(h)), "tag_sfb_plan")
+        self._h = h
+
+    # dtypes as torch dtypes
+    @property
+    def in_torch(self):
+        return _TORCH_DT[self.in_dtype]
+
+    @property
+    def out_torch(self):
+        return _TORCH_DT[self.out_dtype]
+
+    def _xy(self, X, dY):
+        return (_dev(X, self.in_torch, (self.B, self.M), "X"),
+                _dev(dY, self.in_torch, (self.B, self.N), "dY"))
+
+    def sync(self, X, dY, dW, stream=None):
+        x, dy = self._xy(X, dY)
+        _check(_lib.tag_sfb_sync(self._h, x, dy, _dev(dW, self.out_torch, (self.M, self.N), "dW"),
+                                 _stream(stream)), "tag_sfb_sync")
+        return dW
+
+    def gather(self, X, dY, stream=None):
+        x, dy = self._xy(X, dY)
+        _check(_lib.tag_sfb_gather(self._h, x, dy, _stream(stream)), "tag_sfb_gather")
+
+    def reconstruct(self, dW, stream=None):
+        _check(_lib.tag_sfb_reconstruct(self._h, _dev(dW, self.out_torch, (self.M, self.N), "dW"),
+                                        _stream(stream)), "tag_sfb_reconstruct")
+        return dW
+
+    def sync_sgd(self, X, dY, W, v, dW=None, stream=None):
+        x, dy = self._xy(X, dY)
+        shape = (self.M, self.N)
+        dw = _dev(dW, self.out_torch, shape, "dW") if dW is not None else _vp()
+        _check(_lib.tag_sfb_sync_sgd(self._h, x, dy, _dev(W, torch.float32, shape, "W"),
+                                     _dev(v, torch.float32, shape, "v"), dw, _stream(stream)),
+               "tag_sfb_sync_sgd")
+
+    def sync_host(self, X_host, dY_host, dW_host, stream=None):
+        _check(_lib.tag_sfb_sync_host(
+            self._h, _host(X_host, self.in_torch, (self.B, self.M), "X_host"),
+            _host(dY_host, self.in_torch, (self.B, self.N), "dY_host"),
+            _host(dW_host, self.out_torch, (self.M, self.N), "dW_host"), _stream(stream)),
+            "tag_sfb_sync_host")
+        return dW_host
+
+    def local_grad(self, X, dY, dW, stream=None):
+        x, dy = self._xy(X, dY)
+        _check(_lib.tag_local_grad(self._h, x, dy, _dev(dW, self.out_torch, (self.M, self.N), "dW"),
+                                   _stream(stream)), "tag_local_grad")
+        return dW
+
+    def dense_allreduce(self, dW, stream=None):
+        _check(_lib.tag_dense_allreduce(self._h, _dev(dW, self.out_torch, (self.M, self.N), "dW"),
+                                        _stream(stream)), "tag_dense_allreduce")
+        return dW
+
+    def sgd_step(self, dW, W, v, stream=None):
+        shape = (self.M, self.N)
+        _check(_lib.tag_sgd_step(self._h, _dev(dW, torch.float32, shape, "dW"),
+                                 _dev(W, torch.float32, shape, "W"),
+                                 _dev(v, torch.float32, shape, "v"), _stream(stream)),
+               "tag_sgd_step")
+
+    def close(self):
+        if self._h:
+            _check(_lib.tag_sfb_plan_destroy(self._h), "tag_sfb_plan_destroy")
+            self._h = None
+
+
+def select(layers, n, link_bytes_per_s=900_000_000_000, tensor_flops=0, rule=RULE_NORTHSTAR):
+    """Per-layer choice (SYNC_SFB / SYNC_ALLREDUCE / SYNC_NONE). layers: iterable of dicts with
+    M, N, B and optional factor_dtype / grad_dtype ("bf16" | "f32")."""
+    layers = list(layers)
+    arr = (LayerDesc * max(1, len(layers)))()
+    for i, L in enumerate(layers):
+        arr[i] = LayerDesc(L["M"], L["N"], L["B"], _DT_OF[L.get("factor_dtype", "bf16")],
+                           _DT_OF[L.get("grad_dtype", "f32")])
+    topo = Topology(n, link_bytes_per_s, tensor_flops, rule)
+    out = (ctypes.c_int * max(1, len(layers)))()
+    _check(_lib.tag_sfb_select(arr, len(layers), ctypes.byref(topo), out), "tag_sfb_select")
+    return [out[i] for i in range(len(layers))]

@@ -1,0 +1,121 @@
+"""C-ABI checks that need no GPU: the library loads, exports every function include/tag.h declares,
+the host-only selector is bit-exact against the oracle, and argument validation fails cleanly."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def tagmod():
+    from paper_2302_06126_b200 import tag
+    return tag
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "tag.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(tag_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(tagmod):
+    declared = _declared_functions()
+    assert len(declared) >= 19
+    for name in declared:
+        assert hasattr(tagmod._lib, name), name
+    assert set(declared) == set(tagmod.EXPORTS)
+
+
+def test_exports_match_nm(tagmod):
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", tagmod.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (tag_[a-z0-9_]+)", out))
+    assert exported == set(_declared_functions())
+    # the library is built for sm_100a only
+    sass = subprocess.run(["cuobjdump", "--list-elf", tagmod.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    assert "sm_100a" in sass
+
+
+def test_version_and_status_strings(tagmod):
+    assert "sm_100a" in tagmod.version()
+    assert tagmod._lib.tag_status_string(tagmod.ERR_INVALID_ARG) == b"TAG_ERR_INVALID_ARG"
+    assert tagmod._lib.tag_status_string(99) == b"TAG_ERR_UNKNOWN"
+
+
+def test_select_matches_oracle_appendix_a(tagmod, oracle_mod):
+    import json
+    S = oracle_mod.selector
+    cases = json.load(open(os.path.join(ROOT, "tests", "golden", "appendix_a_decisions.json")))
+    for c in cases["cases"]:
+        lay = dict(M=c["M"], N=c["N"], B=c["B"], factor_dtype="f32" if c["e_w"] == 4 else "bf16",
+                   grad_dtype="f32" if c["e_g"] == 4 else "bf16")
+        got = tagmod.select([lay], c["n"], c["tau"], c["F"], c["rule"])[0]
+        want = S.select(dict(M=c["M"], N=c["N"], B=c["B"], e_w=c["e_w"], e_g=c["e_g"]),
+                        dict(n=c["n"], tau=c["tau"], F=c["F"], rule=c["rule"]))
+        assert got == want, c
+
+
+def test_select_random_bit_exact(tagmod, oracle_mod):
+    S = oracle_mod.selector
+    rs = np.random.default_rng(11)
+    for _ in range(400):
+        L = int(rs.integers(1, 6))
+        lays = [dict(M=int(rs.integers(1, 60000)), N=int(rs.integers(1, 60000)),
+                     B=int(rs.integers(1, 4096)), e_w=int(rs.choice([2, 4])),
+                     e_g=int(rs.choice([2, 4]))) for _ in range(L)]
+        n = int(rs.integers(1, 65))
+        tau = int(rs.integers(1, 2 * 10 ** 12))
+        F = int(rs.choice([0, int(rs.integers(1, 4 * 10 ** 15))]))
+        rule = int(rs.integers(0, 3))
+        dt = {2: "bf16", 4: "f32"}
+        got = tagmod.select([dict(M=l["M"], N=l["N"], B=l["B"], factor_dtype=dt[l["e_w"]],
+                                  grad_dtype=dt[l["e_g"]]) for l in lays], n, tau, F, rule)
+        want = [S.select(l, dict(n=n, tau=tau, F=F, rule=rule)) for l in lays]
+        assert got == want
+
+
+def test_select_knife_edges(tagmod, oracle_mod):
+    """Exact ties and one-unit neighbours: the library must agree with exact arithmetic."""
+    S = oracle_mod.selector
+    # tie (S:506 -> AllReduce): n^2 S = 2(n-1) G at M = N = 16, B = 4, bf16/bf16, n = 2
+    assert tagmod.select([dict(M=16, N=16, B=4, factor_dtype="bf16", grad_dtype="bf16")], 2,
+                         10 ** 9, 0)[0] == tagmod.SYNC_ALLREDUCE
+    assert tagmod.select([dict(M=16, N=16, B=3, factor_dtype="bf16", grad_dtype="bf16")], 2,
+                         10 ** 9, 0)[0] == tagmod.SYNC_SFB
+    # Transformer FFN at n = 4 with the compute term: 6.96 us vs 6.99 us
+    lay = dict(M=512, N=2048, B=256)
+    for F in (1421400000000000, 10 ** 15, 2 * 10 ** 15):
+        for tau in (9 * 10 ** 11, 8 * 10 ** 11, 77 * 10 ** 10):
+            got = tagmod.select([dict(lay, factor_dtype="bf16", grad_dtype="f32")], 4, tau, F)[0]
+            assert got == S.select(dict(lay, e_w=2, e_g=4), dict(n=4, tau=tau, F=F))
+
+
+def test_select_n1_and_errors(tagmod):
+    assert tagmod.select([dict(M=4, N=4, B=1)], 1) == [tagmod.SYNC_NONE]
+    with pytest.raises(tagmod.TagError) as e:
+        tagmod.select([dict(M=0, N=4, B=1)], 2)
+    assert e.value.status == tagmod.ERR_INVALID_ARG
+    with pytest.raises(tagmod.TagError):
+        tagmod.select([dict(M=4, N=4, B=1)], 2, link_bytes_per_s=0)
+    with pytest.raises(tagmod.TagError):
+        tagmod.select([dict(M=4, N=4, B=1)], 2, rule=7)
+    assert tagmod.select([], 2) == []
+    # overflow is reported, never wrapped
+    with pytest.raises(tagmod.TagError) as e:
+        tagmod.select([dict(M=2 ** 40, N=2 ** 40, B=2 ** 30)], 64, 2 ** 63, 2 ** 63)
+    assert e.value.status == tagmod.ERR_UNSUPPORTED
+
+
+def test_no_gpu_means_loud_failure(tagmod):
+    """Without a CUDA device the compute path must fail, never fall back to the CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(tagmod.TagError) as e:
+        tagmod.Comm(1, 0, 0)
+    assert e.value.status in (tagmod.ERR_CUDA, tagmod.ERR_INVALID_ARG)

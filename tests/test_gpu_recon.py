@@ -1,0 +1,261 @@
+"""GPU parity of the single-GPU SFB path through the C ABI (`-m gpu`): reconstruction (tcgen05 and
+SIMT kernels), pack/cast, epilogues E1/E2, dense local gradient, host-buffer e2e form, edge cases.
+
+Virtual-n: NCCL cannot put two ranks on one GPU, so the n-replica reconstruction
+is exercised with a 1-rank plan whose B' = n*B rows are the n replicas' factors stacked
+rank-major — the same K = nB contraction and the same alpha = 1/(nB) as after the all-gather.
+Tolerances (north_star; DESIGN "Parity"): bit-exact on small-integer inputs; relative Frobenius
+<= 1e-5 against the oracle fed the exact operand values; <= 2e-2 against the user's fp32 values
+for bf16 wire factors.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2302_06126_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+TORCH = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+def rel_fro(a, r):
+    a = np.asarray(a, np.float64)
+    r = np.asarray(r, np.float64)
+    return float(np.linalg.norm(a - r) / max(np.linalg.norm(r), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def comm1(tag, cuda):
+    c = tag.Comm(1, 0, 0)
+    yield c
+    c.close()
+
+
+def to_dev(a, dt):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(TORCH[dt]).to("cuda")
+
+
+def exact_values(a, dt):
+    """The values the GPU operates on (fp32 -> bf16 is torch RNE), as fp64."""
+    return torch.from_numpy(np.ascontiguousarray(a)).to(TORCH[dt]).double().numpy()
+
+
+def run_sync(tag, comm, Xall, dYall, in_dt="bf16", wire_dt="bf16", out_dt="f32"):
+    K, M = Xall.shape
+    N = dYall.shape[1]
+    plan = tag.SfbPlan(comm, M, N, K, in_dt, wire_dt, out_dt)
+    dW = torch.full((M, N), float("nan"), dtype=TORCH[out_dt], device="cuda")
+    plan.sync(to_dev(Xall, in_dt), to_dev(dYall, in_dt), dW)
+    torch.cuda.synchronize()
+    plan.close()
+    return dW
+
+
+def expected_int(oracle_mod, Xall, dYall, n_times_b, out_dt):
+    """Bit pattern the epilogue must produce for integer inputs: fl32(S * fl32(1/(nB))) and, for a
+    bf16 output, RNE of that fp32 value (DESIGN "Parity")."""
+    S = oracle_mod.sfb_sum(Xall[None], dYall[None])
+    assert np.all(np.abs(S) < 2 ** 24)           # fp32 accumulation is exact
+    e = S.astype(np.float32) * np.float32(1.0 / n_times_b)
+    if out_dt == "f32":
+        return e
+    return oracle_mod.bf16_bits_to_f64(oracle_mod.cast_bf16_bits(e)).astype(np.float32)
+
+
+# tensor-core shapes (M, N multiples of 8) and SIMT shapes (odd), K = n*B with ragged tails
+TC_SHAPES = [(64, 32, 8), (128, 256, 32), (136, 264, 40), (520, 1000, 64), (1024, 4096, 256),
+             (256, 512, 5), (8, 8, 1), (384, 768, 2048), (4096, 1000, 256)]
+SIMT_SHAPES = [(1, 1, 2), (3, 5, 6), (17, 33, 12), (130, 257, 10)]
+
+
+@pytest.mark.parametrize("M,N,K", TC_SHAPES + SIMT_SHAPES)
+@pytest.mark.parametrize("out_dt", ["f32", "bf16"])
+def test_integer_inputs_bit_exact(tag, comm1, oracle_mod, M, N, K, out_dt):
+    X = synth.draw("int3", K, M, synth.rng(50, M, N, 0))
+    dY = synth.draw("int3", K, N, synth.rng(50, M, N, 1))
+    dW = run_sync(tag, comm1, X, dY, "bf16", "bf16", out_dt).float().cpu().numpy()
+    want = expected_int(oracle_mod, X, dY, K, out_dt)
+    assert np.array_equal(dW.view(np.uint32), want.view(np.uint32)), \
+        f"max |diff| {np.abs(dW - want).max()}"
+
+
+@pytest.mark.parametrize("n,B", [(1, 32), (2, 32), (4, 32), (8, 32), (8, 64)])
+def test_virtual_n_random_vgg_fc7(tag, comm1, oracle_mod, n, B):
+    """VGG-19 fc7 shape (4096 x 4096) at K = n*B: post-ReLU X, masked small dY (d-2 recipe)."""
+    X, dY = synth.all_factors(2, 7, n, 4096, 4096, B, "relu", "masked_small")
+    Xall, dYall = X.reshape(n * B, 4096), dY.reshape(n * B, 4096)
+    dW = run_sync(tag, comm1, Xall, dYall).cpu().numpy()
+    ref_exact = oracle_mod.sfb_dw(exact_values(X, "bf16"), exact_values(dY, "bf16"))
+    ref_user = oracle_mod.sfb_dw(X, dY)
+    assert rel_fro(dW, ref_exact) <= 1e-5
+    assert rel_fro(dW, ref_user) <= 2e-2
+
+
+def test_fp32_toy_config(tag, comm1, oracle_mod):
+    """Config 1: M=64, N=32, B=4, n=2, fp32 end to end (SIMT FFMA path): <= 1e-5."""
+    X, dY = synth.all_factors(1, 0, 2, 64, 32, 4, "normal", "normal")
+    dW = run_sync(tag, comm1, X.reshape(8, 64), dY.reshape(8, 32), "f32", "f32", "f32")
+    assert rel_fro(dW.cpu().numpy(), oracle_mod.sfb_dw(X, dY)) <= 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 2048, 256), (100, 36, 7)])
+def test_fp32_wire_random(tag, comm1, oracle_mod, M, N, K):
+    X = synth.draw("normal", K, M, synth.rng(51, M, N, 0))
+    dY = synth.draw("normal", K, N, synth.rng(51, M, N, 1))
+    dW = run_sync(tag, comm1, X, dY, "f32", "f32", "f32")
+    assert rel_fro(dW.cpu().numpy(), oracle_mod.sfb_dw(X[None], dY[None])) <= 1e-5
+
+
+def test_pack_cast_is_rne(tag, comm1, oracle_mod):
+    """fp32 inputs, bf16 wire: with dY = identity rows, dW[m][b] = alpha * bf16(X[b][m]) exactly,
+    so the pack kernel's cast is compared bit for bit with the oracle's RNE cast."""
+    K, M = 16, 4104                                # 4104*16 = 65664 values incl. vector tail
+    X = synth.draw("normal", K, M, synth.rng(52, 0, 0, 0))
+    X[0, :8] = [1 + 2 ** -8, 1 + 3 * 2 ** -8, -(1 + 2 ** -8), 2 ** -120, 3.0e38, 0.0, -1.5, 1.0]   # all finite in bf16
+    dY = np.eye(K, dtype=np.float32)
+    dW = run_sync(tag, comm1, X, dY, "f32", "bf16", "f32").cpu().numpy()   # M x K
+    cast = oracle_mod.bf16_bits_to_f64(oracle_mod.cast_bf16_bits(X)).astype(np.float32)
+    want = (cast.T * np.float32(1.0 / K)).astype(np.float32)
+    assert np.array_equal(dW.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("M,N,K", [(4096, 1000, 32), (25088, 4096, 32)])
+def test_full_size_sampled(tag, comm1, oracle_mod, M, N, K):
+    """VGG-19 fc8 / fc6 at n = 1, B = 32 — the bench's launch configuration. 4000 sampled entries
+    against the oracle computed one by one, plus whole-matrix properties."""
+    layer = {1000: 8, 4096: 6}[N]
+    X, dY = synth.all_factors(2, layer, 1, M, N, K, "relu",
+                              "softmax_onehot" if N == 1000 else "masked_small")
+    dW = run_sync(tag, comm1, X[0], dY[0]).cpu().numpy()
+    idx = np.random.default_rng(7).integers(0, M * N, 4000)
+    Xe, dYe = exact_values(X, "bf16"), exact_values(dY, "bf16")
+    ref = oracle_mod.sfb_sum_entries(Xe, dYe, idx) / K
+    assert rel_fro(dW.ravel()[idx], ref) <= 1e-5
+    assert np.isfinite(dW).all()
+    # rank <= K property, checked on a random sketch of the whole matrix
+    g = torch.Generator(device="cuda").manual_seed(0)
+    sketch = torch.from_numpy(dW).cuda().double() @ torch.randn(N, 2 * K, device="cuda",
+                                                                dtype=torch.float64, generator=g)
+    s = torch.linalg.svdvals(sketch).cpu().numpy()
+    assert s[K] / s[0] < 1e-5
+
+
+def test_local_grad_and_dense_n1(tag, comm1, oracle_mod):
+    M, N, B = 1024, 512, 48
+    X = synth.draw("int3", B, M, synth.rng(53, 0, 0, 0))
+    dY = synth.draw("int3", B, N, synth.rng(53, 0, 0, 1))
+    plan = tag.SfbPlan(comm1, M, N, B, "bf16", "bf16", "f32")
+    Xd, dYd = to_dev(X, "bf16"), to_dev(dY, "bf16")
+    loc = torch.empty(M, N, device="cuda")
+    plan.local_grad(Xd, dYd, loc)
+    torch.cuda.synchronize()
+    S = oracle_mod.sfb_sum(X[None], dY[None])
+    assert np.array_equal(loc.cpu().numpy(), S.astype(np.float32))        # unscaled, exact
+    plan.dense_allreduce(loc)                                             # n = 1: dW <- dW / B
+    sfb = torch.empty(M, N, device="cuda")
+    plan.sync(Xd, dYd, sfb)
+    torch.cuda.synchronize()
+    assert torch.equal(loc, sfb)
+    plan.close()
+
+
+def test_fused_sgd_matches_unfused_and_oracle(tag, comm1, oracle_mod):
+    """E2: the fused epilogue equals reconstruct + tag_sgd_step bit for bit, and the fp64 oracle
+    (BERT-L pooler shape, virtual n = 8, B = 2; lr 1e-3, mu 0.9, wd 1e-2)."""
+    n, B, M, N = 8, 2, 1024, 1024
+    X, dY = synth.all_factors(5, 3, n, M, N, B, "tanh", "small")
+    W0, v0 = synth.sgd_state(5, 3, M, N)
+    v0 = (v0 + 1e-4 * synth.draw("normal", M, N, synth.rng(5, 3, 0, 9))).astype(np.float32)
+    hp = dict(lr=1e-3, momentum=0.9, weight_decay=1e-2)
+    plan = tag.SfbPlan(comm1, M, N, n * B, "bf16", "bf16", "f32", fuse_sgd=True, **hp)
+    Xd, dYd = to_dev(X.reshape(n * B, M), "bf16"), to_dev(dY.reshape(n * B, N), "bf16")
+    W1, v1 = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
+    dW1 = torch.empty(M, N, device="cuda")
+    plan.sync_sgd(Xd, dYd, W1, v1, dW1)
+    W2, v2 = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
+    dW2 = torch.empty(M, N, device="cuda")
+    plan.sync(Xd, dYd, dW2)
+    plan.sgd_step(dW2, W2, v2)
+    W3, v3 = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
+    plan.sync_sgd(Xd, dYd, W3, v3, None)                 # no dW write at all
+    torch.cuda.synchronize()
+    assert torch.equal(dW1, dW2) and torch.equal(W1, W2) and torch.equal(v1, v2)
+    assert torch.equal(W1, W3) and torch.equal(v1, v3)
+    g = oracle_mod.sfb_dw(exact_values(X, "bf16"), exact_values(dY, "bf16"))
+    Wr, vr = oracle_mod.sgd_momentum(g, W0, v0, hp["lr"], hp["momentum"], hp["weight_decay"])
+    assert rel_fro(v1.cpu().numpy(), vr) <= 1e-5
+    # W' = W - lr*v is rounded to fp32 once per element: at most 1 ulp(W') plus the v error
+    W1n = W1.cpu().numpy()
+    tol = np.spacing(np.abs(Wr).astype(np.float32)) + hp["lr"] * (1e-5 * np.abs(vr) + 1e-12)
+    assert np.all(np.abs(W1n - Wr) <= tol)
+    assert rel_fro(W1n, Wr) <= 1e-6
+    plan.close()
+
+
+def test_sync_host_matches_device(tag, comm1):
+    M, N, B = 4096, 1000, 32
+    X, dY = synth.factors(2, 8, 0, M, N, B, "relu", "softmax_onehot")
+    plan = tag.SfbPlan(comm1, M, N, B, "bf16", "bf16", "f32")
+    Xh = torch.from_numpy(X).to(torch.bfloat16).pin_memory()
+    dYh = torch.from_numpy(dY).to(torch.bfloat16).pin_memory()
+    dWh = torch.empty(M, N).pin_memory()
+    plan.sync_host(Xh, dYh, dWh)
+    dWd = torch.empty(M, N, device="cuda")
+    plan.sync(Xh.cuda(), dYh.cuda(), dWd)
+    torch.cuda.synchronize()
+    assert torch.equal(dWh, dWd.cpu())
+    plan.close()
+
+
+def test_stage_split_equals_sync(tag, comm1):
+    M, N, B = 512, 2048, 256
+    X, dY = synth.factors(4, 2, 0, M, N, B, "normal", "small")
+    plan = tag.SfbPlan(comm1, M, N, B, "f32", "bf16", "bf16")
+    Xd, dYd = to_dev(X, "f32"), to_dev(dY, "f32")
+    a = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+    b = torch.empty_like(a)
+    plan.sync(Xd, dYd, a)
+    plan.gather(Xd, dYd)
+    plan.reconstruct(b)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    plan.close()
+
+
+def test_invalid_arguments_have_no_side_effects(tag, comm1):
+    with pytest.raises(tag.TagError) as e:
+        tag.SfbPlan(comm1, 0, 4, 4)
+    assert e.value.status == tag.ERR_INVALID_ARG
+    plan = tag.SfbPlan(comm1, 64, 32, 8)
+    X = torch.zeros(8, 64, dtype=torch.bfloat16, device="cuda")
+    dY = torch.zeros(8, 32, dtype=torch.bfloat16, device="cuda")
+    dW = torch.full((64, 32), 7.0, device="cuda")
+    before = tag.kernel_launches()
+    st = tag._lib.tag_sfb_sync(plan._h, tag._vp(X.data_ptr() + 2), tag._vp(dY.data_ptr()),
+                               tag._vp(dW.data_ptr()), tag._vp(0))
+    assert st == tag.ERR_INVALID_ARG
+    st = tag._lib.tag_sfb_sync(plan._h, tag._vp(0), tag._vp(dY.data_ptr()),
+                               tag._vp(dW.data_ptr()), tag._vp(0))
+    assert st == tag.ERR_INVALID_ARG
+    torch.cuda.synchronize()
+    assert tag.kernel_launches() == before and torch.all(dW == 7.0)
+    # reconstruct before any gather on a fresh plan is an error, not garbage
+    with pytest.raises(tag.TagError):
+        plan.reconstruct(dW)
+    with pytest.raises(tag.TagError):
+        plan.sync_sgd(X, dY, torch.zeros(64, 32, device="cuda"), torch.zeros(64, 32, device="cuda"))
+    plan.close()
+
+
+def test_launch_counter_counts_kernels(tag, comm1):
+    plan = tag.SfbPlan(comm1, 4096, 1000, 32)
+    X = torch.ones(32, 4096, dtype=torch.bfloat16, device="cuda")
+    dY = torch.ones(32, 1000, dtype=torch.bfloat16, device="cuda")
+    dW = torch.empty(4096, 1000, device="cuda")
+    before = tag.kernel_launches()
+    plan.sync(X, dY, dW)
+    torch.cuda.synchronize()
+    assert tag.kernel_launches() - before == 1          # n = 1, bf16 in == wire: recon only
+    assert torch.all(dW == 1.0)                          # X = dY = 1 -> dW = 1 (scale pin)
+    plan.close()
