@@ -36,6 +36,7 @@ from paper_2302_06126_b200 import synth  # noqa: E402
 
 METRIC = "per-layer SFB grad-sync us & dW GB/s (VGG-19 fc6/fc7/fc8, B=32/GPU)"
 ESIZE = {"f32": 4, "bf16": 2}
+SPIN_CYCLES = 80_000   # torch.cuda._sleep before each start event (not a libtag kernel)
 
 
 def load_peaks():
@@ -49,7 +50,7 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 100 ms during the timed region."""
+    """`nvidia-smi -lms 50` clocks / throttle reasons sampled during the timed region."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -57,42 +58,47 @@ class ClockSampler:
     def __init__(self, index):
         self.index = index
         self.rows = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.1)
+        self._p = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                        "--format=csv,noheader,nounits", "-lms", "50"],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)      # let the first sample land before the timed region starts
+        except OSError:
+            self._p = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        time.sleep(0.06)
+        self._p.terminate()
+        try:
+            out, _ = self._p.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self._p.kill()
+            out, _ = self._p.communicate()
+        self.rows = [[c.strip() for c in ln.split(",")] for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
-        if not self.rows:
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        rows = [r for r in self.rows if len(r) >= 9]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
                     "samples": 0}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [v for v in (num(r[1]) for r in rows) if v is not None]
+        mx = [v for v in (num(r[2]) for r in rows) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows)}
 
 
 def cpu_oracle_baseline(cfg, n, budget_mac=2.5e10):
@@ -147,13 +153,13 @@ def config_json(cfg, n, args):
             "layers": [f"{L.name} {L.M}x{L.N}" for L in cfg.layers], "rows_per_gpu": cfg.layers[0].B,
             "n": n, "in/wire/out": f"{cfg.in_dtype}/{cfg.wire_dtype}/{cfg.out_dtype}",
             "parallelism": f"dp{n} (SFB all-gather + replicated reconstruction)",
-            "l2": "flushed between timed steps (256 MiB write), outside the timed interval"}
+            "l2": "flushed between timed steps (256 MiB write + 256 MiB read), outside the timed interval"}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="tag", choices=["tag", "reference"])
@@ -188,6 +194,13 @@ def main():
                                grad_dtype=cfg.out_dtype) for l in layers], n,
                          900_000_000_000, int(peaks.get("bf16_tflops_sustained", 1400) * 1e12))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    flush_rd = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def flush_l2():
+        # write 256 MiB (> 126 MB L2), then read another 256 MiB so the dirty lines of the write
+        # are drained to HBM before the timed interval starts (outside the events)
+        flush.zero_()
+        flush_rd.sum()
     nl = len(layers)
 
     def step(evs=None):
@@ -204,10 +217,14 @@ def main():
     def timed_loop(nsteps, staged):
         per_step, per_layer_recon, per_layer_sync = [], [[] for _ in range(nl)], [[] for _ in range(nl)]
         for _ in range(nsteps):
-            flush.zero_()
+            flush_l2()
             torch.cuda.synchronize()
             tdist.barrier()
             evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nl + 1)]
+            with torch.cuda.stream(stream):
+                # a ~40 us spin ahead of the start event lets the host enqueue the whole step, so
+                # the interval measures device time, not Python launch latency
+                torch.cuda._sleep(SPIN_CYCLES)
             evs[0].record(stream)
             step(evs if staged else None)
             if not staged:
@@ -280,10 +297,12 @@ def main():
             L = l["L"]
             t = []
             for _ in range(max(3, min(args.steps, 10))):
-                flush.zero_()
+                flush_l2()
                 torch.cuda.synchronize()
                 tdist.barrier()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(stream):
+                    torch.cuda._sleep(SPIN_CYCLES)
                 e0.record(stream)
                 l["plan"].local_grad(l["X"], l["dY"], l["dW"], stream)
                 l["plan"].dense_allreduce(l["dW"], stream)

@@ -39,16 +39,17 @@ constexpr int BK = 32;                   // factor rows per pipeline stage
 constexpr int NUM_EPI_WARPS = 8;
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;   // 320
 constexpr int CHUNK_BYTES = BK * 128;    // one 128-byte-wide MN chunk of BK rows (4 KB)
-constexpr int EPI_BUF_BYTES = 32 * 128;  // 32 rows x 128 B staging for one TMA store
+constexpr int EPI_BUF_BYTES = 32 * 128;  // 32 rows x 128 B transpose buffer per epilogue warp
 constexpr int TMEM_COLS = 512;
 
 template <int BN>
 struct Cfg {
+    static constexpr int ACC = TMEM_COLS / BN;            // accumulator buffers in TMEM
     static constexpr int A_BYTES = (BM / 64) * CHUNK_BYTES;
     static constexpr int B_BYTES = (BN / 64) * CHUNK_BYTES;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES = BN == 256 ? 6 : 8;
-    static constexpr int EPI_BYTES = NUM_EPI_WARPS * 2 * EPI_BUF_BYTES;
+    static constexpr int EPI_BYTES = NUM_EPI_WARPS * EPI_BUF_BYTES;
     static constexpr int BAR_BYTES = 256;
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
     // kind::f16 instruction descriptor: D f32, A/B bf16, both MN-major, N = BN, M = 128.
@@ -61,10 +62,10 @@ struct Params {
     int M, N, K;
     int num_n_blocks, num_tiles, num_k_blocks;
     float alpha;
+    void* C;          // dW out (may be nullptr with SGD)
     float* W;
     float* V;
     float lr, mu, wd;
-    int write_dw;
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -72,10 +73,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
+__device__ __forceinline__ void grid_dep_wait() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void grid_dep_launch() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 template <int BN, bool OUT_BF16, bool SGD>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const __grid_constant__ CUtensorMap tmC, const Params p)
+                const Params p)
 {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
@@ -86,9 +94,9 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t s_bar = s_epi + C::EPI_BYTES;
     const uint32_t bar_full = s_bar;                       // [STAGES]
     const uint32_t bar_empty = s_bar + 8 * C::STAGES;      // [STAGES]
-    const uint32_t bar_tfull = s_bar + 16 * C::STAGES;     // [2]
-    const uint32_t bar_tempty = bar_tfull + 16;            // [2]
-    const uint32_t s_tmem_slot = bar_tempty + 16;
+    const uint32_t bar_tfull = s_bar + 16 * C::STAGES;     // [ACC]
+    const uint32_t bar_tempty = bar_tfull + 8 * C::ACC;    // [ACC]
+    const uint32_t s_tmem_slot = bar_tempty + 8 * C::ACC;
     uint8_t* gen_base = smem_raw + (base - ptx::smem_addr(smem_raw));
     volatile uint32_t* tmem_slot_ptr =
         reinterpret_cast<volatile uint32_t*>(gen_base + (s_tmem_slot - base));
@@ -96,15 +104,15 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
 
+    // ---- prologue (overlaps the previous kernel's tail under programmatic dependent launch)
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
         ptx::tma_prefetch_desc(&tmB);
-        if (!SGD || p.write_dw) ptx::tma_prefetch_desc(&tmC);
         for (int s = 0; s < C::STAGES; ++s) {
             ptx::mbar_init(bar_full + 8 * s, 1);
             ptx::mbar_init(bar_empty + 8 * s, 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < C::ACC; ++a) {
             ptx::mbar_init(bar_tfull + 8 * a, 1);
             ptx::mbar_init(bar_tempty + 8 * a, NUM_EPI_WARPS);
         }
@@ -115,6 +123,8 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot_ptr;
+    // no global memory is touched before the previous grid in the stream has completed
+    grid_dep_wait();
 
     if (warp == 0) {
         // ===================================================== TMA producer
@@ -167,21 +177,28 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
                 ptx::mma_commit(bar_tfull + 8 * acc);                   // accumulator ready
-                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+                if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
             }
+            // all MMAs of this CTA are issued: let the next kernel in the stream start launching
+            grid_dep_launch();
         }
     } else {
         // ===================================================== epilogue warps
+        // TMEM -> registers (one output row per lane) -> scale -> 128B-swizzled smem transpose
+        // -> coalesced 16-byte streaming stores, four full 128-byte lines per warp instruction.
         const int ew = warp - 2;                 // 0..7
         const int quad = warp & 3;               // TMEM lane quadrant this warp may access
         const int half = ew >> 2;                // which half of the tile's columns
-        const uint32_t my_buf = s_epi + ew * 2 * EPI_BUF_BYTES;
-        int buf = 0;
+        const uint32_t sbuf = s_epi + ew * EPI_BUF_BYTES;
+        constexpr int ESZ = OUT_BF16 ? 2 : 4;
+        constexpr int COLS_PER_CHUNK = 128 / ESZ;               // 128 bytes of output per row
+        constexpr int CHUNKS = (BN / 2) / COLS_PER_CHUNK;
+        constexpr int VEC = 16 / ESZ;                           // output elements per 16 B
+        const float alpha = p.alpha;
+        const int sub = lane >> 3;               // row within a 4-row group (write-out phase)
+        const int cj = lane & 7;                 // 16-byte column slot (write-out phase)
         int acc = 0;
         uint32_t acc_phase = 0;
-        constexpr int COLS_PER_CHUNK = OUT_BF16 ? 64 : 32;    // 128 bytes of output per row
-        constexpr int CHUNKS = (BN / 2) / COLS_PER_CHUNK;
-        const float alpha = p.alpha;
         for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
             const int m0 = (tile / p.num_n_blocks) * BM;
             const int n0 = (tile % p.num_n_blocks) * BN;
@@ -189,10 +206,17 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
             ptx::tc_fence_after();
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quad) << 16) + acc * BN;
+            // chunks of this warp's column half that hold any output column (warp-uniform)
+            int nch = (p.N - (n0 + half * (BN / 2)) + COLS_PER_CHUNK - 1) / COLS_PER_CHUNK;
+            nch = nch < 0 ? 0 : (nch > CHUNKS ? CHUNKS : nch);
+            if (nch == 0) {                       // nothing to read: release the accumulator
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+            }
 #pragma unroll 1
-            for (int ch = 0; ch < CHUNKS; ++ch) {
+            for (int ch = 0; ch < nch; ++ch) {
                 const int col = half * (BN / 2) + ch * COLS_PER_CHUNK;   // within the tile
-                if (n0 + col >= p.N) break;                              // warp-uniform
                 uint32_t w[32];                                          // 128 B of this row
                 if constexpr (OUT_BF16) {
                     uint32_t r0[32], r1[32];
@@ -207,81 +231,61 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                                                 __fmul_rn(__uint_as_float(r1[2 * i + 1]), alpha));
                     }
                 } else {
-                    uint32_t r[32];
-                    ptx::tmem_ld_32x32b_x32(t_row + col, r);
+                    ptx::tmem_ld_32x32b_x32(t_row + col, w);
                     ptx::tmem_wait_ld();
-                    if constexpr (SGD) {
-                        // E2: g = alpha*acc + wd*W ; v = mu*v + g ; W -= lr*v   (fp32, R14)
-                        const int grow = row0 + static_cast<int>(lane);
-                        const int gcol = n0 + col;
-                        if (grow < p.M) {
-                            float* wp = p.W + static_cast<int64_t>(grow) * p.N + gcol;
-                            float* vp = p.V + static_cast<int64_t>(grow) * p.N + gcol;
-                            const int nvalid = min(32, p.N - gcol);
-                            if (nvalid == 32) {
-                                float4 wv[8], vv[8];
-#pragma unroll
-                                for (int i = 0; i < 8; ++i) {
-                                    wv[i] = reinterpret_cast<const float4*>(wp)[i];
-                                    vv[i] = reinterpret_cast<const float4*>(vp)[i];
-                                }
-#pragma unroll
-                                for (int i = 0; i < 8; ++i) {
-                                    float* wf = reinterpret_cast<float*>(&wv[i]);
-                                    float* vf = reinterpret_cast<float*>(&vv[i]);
-#pragma unroll
-                                    for (int e = 0; e < 4; ++e) {
-                                        const float d = __fmul_rn(__uint_as_float(r[4 * i + e]), alpha);
-                                        const float g = __fadd_rn(d, __fmul_rn(p.wd, wf[e]));
-                                        vf[e] = __fadd_rn(__fmul_rn(p.mu, vf[e]), g);
-                                        wf[e] = __fsub_rn(wf[e], __fmul_rn(p.lr, vf[e]));
-                                    }
-                                }
-#pragma unroll
-                                for (int i = 0; i < 8; ++i) {
-                                    reinterpret_cast<float4*>(wp)[i] = wv[i];
-                                    reinterpret_cast<float4*>(vp)[i] = vv[i];
-                                }
-                            } else {
-                                for (int e = 0; e < nvalid; ++e) {
-                                    const float d = __fmul_rn(__uint_as_float(r[e]), alpha);
-                                    const float g = __fadd_rn(d, __fmul_rn(p.wd, wp[e]));
-                                    const float vn = __fadd_rn(__fmul_rn(p.mu, vp[e]), g);
-                                    vp[e] = vn;
-                                    wp[e] = __fsub_rn(wp[e], __fmul_rn(p.lr, vn));
-                                }
-                            }
-                        }
-                        if (!p.write_dw) continue;
-                    }
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
-                        w[i] = __float_as_uint(__fmul_rn(__uint_as_float(r[i]), alpha));
+                        w[i] = __float_as_uint(__fmul_rn(__uint_as_float(w[i]), alpha));
                 }
-                // staging buffer free? (its previous TMA store has finished reading smem)
-                if (lane == 0) ptx::bulk_wait_read<1>();
-                __syncwarp();
-                const uint32_t sbuf = my_buf + buf * EPI_BUF_BYTES;
+                if (ch == nch - 1) {
+                    // last TMEM read of this accumulator by this warp: hand it back to the MMA
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+                }
+                __syncwarp();                     // previous chunk's smem reads are done
                 const uint32_t rowaddr = sbuf + lane * 128;
 #pragma unroll
-                for (int j = 0; j < 8; ++j)   // 16-byte chunk j of this row, 128B-swizzled
+                for (int j = 0; j < 8; ++j)       // 16-byte slot j of row `lane`, swizzled
                     ptx::st_shared_v4(rowaddr + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1],
                                       w[4 * j + 2], w[4 * j + 3]);
-                ptx::fence_async_smem();
                 __syncwarp();
-                if (lane == 0) {
-                    ptx::tma_store_2d(&tmC, sbuf, n0 + col, row0);
-                    ptx::bulk_commit();
+                const int gcol = n0 + col + cj * VEC;
+                const bool col_ok = gcol < p.N;   // N % 8 == 0: a 16-byte slot is all in or out
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int r = 4 * i + sub;
+                    const int grow = row0 + r;
+                    uint32_t a, b, c, d;
+                    ptx::ld_shared_v4(sbuf + r * 128 + ((cj ^ (r & 7)) << 4), a, b, c, d);
+                    if (!col_ok || grow >= p.M) continue;
+                    const int64_t off = static_cast<int64_t>(grow) * p.N + gcol;
+                    if constexpr (SGD) {
+                        // E2 (R14): g = dW + wd*W ; v = mu*v + g ; W -= lr*v   (fp32)
+                        float4* wp = reinterpret_cast<float4*>(p.W + off);
+                        float4* vp = reinterpret_cast<float4*>(p.V + off);
+                        float4 wv = __ldcs(wp);
+                        float4 vv = __ldcs(vp);
+                        const float dv[4] = {__uint_as_float(a), __uint_as_float(b),
+                                             __uint_as_float(c), __uint_as_float(d)};
+                        float* wf = reinterpret_cast<float*>(&wv);
+                        float* vf = reinterpret_cast<float*>(&vv);
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float g = __fadd_rn(dv[e], __fmul_rn(p.wd, wf[e]));
+                            vf[e] = __fadd_rn(__fmul_rn(p.mu, vf[e]), g);
+                            wf[e] = __fsub_rn(wf[e], __fmul_rn(p.lr, vf[e]));
+                        }
+                        __stcs(wp, wv);
+                        __stcs(vp, vv);
+                        if (p.C == nullptr) continue;
+                    }
+                    __stcs(reinterpret_cast<uint4*>(static_cast<uint8_t*>(p.C) + off * ESZ),
+                           make_uint4(a, b, c, d));
                 }
-                buf ^= 1;
             }
-            // all TMEM reads of this accumulator are complete (wait::ld above)
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
         }
-        if (lane == 0) ptx::bulk_wait<0>();
     }
 
     ptx::tc_fence_before();
@@ -322,19 +326,10 @@ bool encode_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esiz
 template <int BN, bool OUT_BF16, bool SGD>
 tag_status_t launch_t(const ReconArgs& a, cudaStream_t s) {
     using C = Cfg<BN>;
-    CUtensorMap tmA, tmB, tmC;
+    CUtensorMap tmA, tmB;
     if (!encode_2d(&tmA, a.A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.K, a.M, 64, BK) ||
         !encode_2d(&tmB, a.Bm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.K, a.N, 64, BK))
         return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
-    const bool write_dw = a.C != nullptr;
-    if (write_dw) {
-        const bool ok = OUT_BF16
-            ? encode_2d(&tmC, a.C, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.M, a.N, 64, 32)
-            : encode_2d(&tmC, a.C, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.M, a.N, 32, 32);
-        if (!ok) return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for dW");
-    } else {
-        tmC = tmA;  // unused
-    }
     Params p;
     p.M = static_cast<int>(a.M);
     p.N = static_cast<int>(a.N);
@@ -344,12 +339,12 @@ tag_status_t launch_t(const ReconArgs& a, cudaStream_t s) {
     p.num_tiles = num_m_blocks * p.num_n_blocks;
     p.num_k_blocks = static_cast<int>((a.K + BK - 1) / BK);
     p.alpha = a.alpha;
+    p.C = a.C;
     p.W = a.W;
     p.V = a.V;
     p.lr = a.lr;
     p.mu = a.mu;
     p.wd = a.wd;
-    p.write_dw = write_dw ? 1 : 0;
     auto kern = recon_tc_kernel<BN, OUT_BF16, SGD>;
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
@@ -358,9 +353,17 @@ tag_status_t launch_t(const ReconArgs& a, cudaStream_t s) {
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recon_tc)");
         attr_set = true;
     }
-    const int grid = p.num_tiles < num_sms() ? p.num_tiles : num_sms();
-    kern<<<grid, NUM_THREADS, C::SMEM, s>>>(tmA, tmB, tmC, p);
-    cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(p.num_tiles < num_sms() ? p.num_tiles : num_sms()));
+    cfg.blockDim = dim3(NUM_THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see kernel)
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, p);
     if (e != cudaSuccess) return cuda_fail(e, "launch recon_tc_kernel");
     count_launch();
     return TAG_OK;
@@ -382,9 +385,10 @@ bool recon_tc_ok(const ReconArgs& a) {
 }
 
 tag_status_t launch_recon_tc(const ReconArgs& a, cudaStream_t s) {
-    // BN = 256 when there are enough tiles to fill every SM at least twice; else BN = 128.
-    const int64_t tiles256 = ((a.M + BM - 1) / BM) * ((a.N + 255) / 256);
-    const bool wide = tiles256 >= 2 * num_sms();
+    // Small K (the HBM-write-bound regime of the paper's small-batch layers): BN = 128 tiles,
+    // 4 TMEM accumulators, finer tail. Large K (tensor-bound): BN = 256 halves the smem operand
+    // traffic per MMA, 2 accumulators.
+    const bool wide = a.K > 256;
     if (a.sgd) return wide ? launch_t<256, false, true>(a, s) : launch_t<128, false, true>(a, s);
     if (a.out == TAG_BF16)
         return wide ? launch_t<256, true, false>(a, s) : launch_t<128, true, false>(a, s);
