@@ -289,7 +289,8 @@ def main():
             "recon_hbm_frac": round(rbytes / (t_rec * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
             "recon_tensor_frac": round(flops / (t_rec * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
             "allgather_busbw_GBps": round(ag / ((t_sync - t_rec) * 1e-3) / 1e9, 1) if n > 1 else None,
-            "selector": {0: "allreduce", 1: "sfb", 2: "none"}[choices[i]]}
+            "selector": {0: "allreduce", 1: "sfb", 2: "none"}[choices[i]],
+            "gather": l["plan"].info()["gather"]}
 
     # ---------------------------------------------------------------- dense baseline (n > 1)
     if n > 1 and not args.no_dense:

@@ -121,10 +121,28 @@ tag_status_t tag_sfb_plan(tag_comm_t comm, const tag_sfb_desc_t* desc, tag_sfb_p
 /* COLLECTIVE. NULL is a no-op. The caller must ensure no work using the plan is still pending. */
 tag_status_t tag_sfb_plan_destroy(tag_sfb_plan_t plan);
 
+/* Which implementation a plan selected (host query, no device work). */
+typedef enum {
+    TAG_GATHER_NONE = 0,        /* n = 1: nothing to exchange                                  */
+    TAG_GATHER_NCCL = 1,        /* pack (if casting) + ncclAllGather                           */
+    TAG_GATHER_NVLINK_PUSH = 2  /* fused pack+push into peers' symmetric windows + LSA barrier */
+} tag_gather_mode_t;
+typedef struct {
+    int tensor_cores;           /* 1: tcgen05 reconstruction; 0: SIMT FFMA (fp32 wire, odd rows) */
+    int gather_mode;            /* tag_gather_mode_t                                            */
+    int64_t K;                  /* n * B                                                        */
+    float alpha;                /* fl32(1/(nB)), the fused epilogue scale                       */
+} tag_plan_info_t;
+tag_status_t tag_sfb_plan_info(tag_sfb_plan_t plan, tag_plan_info_t* out);
+
 /* COLLECTIVE (n > 1). The SFB synchronisation of one layer, steps a1-a4:
  *   a1 pack   : if in_dtype != wire_dtype, RNE-cast X_r and dY_r into this rank's slot of the
  *               gather buffers (16-byte vectorised kernel);
- *   a2 gather : NCCL all-gather of X_r and dY_r over NVLink ("broadcast to all devices");
+ *   a2 gather : X_r and dY_r reach every replica over NVLink ("broadcast to all devices"):
+ *               fused with a1 as a push into the peers' symmetric windows (NCCL device API,
+ *               TAG_GATHER_NVLINK_PUSH), or an ncclAllGather (TAG_GATHER_NCCL) when the rows are
+ *               not 16-byte multiples, the ranks are not all NVLink-reachable, or the environment
+ *               sets TAG_GATHER=nccl;
  *   a3 recon  : dW = alpha * X_all^T dY_all on the tensor cores (K = n*B), alpha = 1/(nB);
  *   a4 store  : dW_out <- dW in out_dtype (fused epilogue).
  * X: B x M, dY: B x N (in_dtype, device). dW_out: M x N (out_dtype, device), overwritten.

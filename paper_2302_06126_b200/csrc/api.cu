@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -14,6 +15,14 @@
 #include "tag_internal.h"
 
 namespace tag {
+// push_gather.cu
+tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, void** out);
+void push_devcomm_destroy(ncclComm_t comm, void* dc);
+bool push_devcomm_all_lsa(const void* dc, int nranks);
+tag_status_t launch_push_gather(const void* dc, ncclWindow_t win, size_t off_x, size_t off_dy,
+                                int slot, const void* X, const void* dY, int64_t cx, int64_t cy,
+                                tag_dtype_t in, tag_dtype_t wire, int max_ctas, cudaStream_t s);
+constexpr int PUSH_MAX_CTAS = 148;
 
 std::atomic<uint64_t> g_launches{0};
 static thread_local std::string t_last_error;
@@ -70,6 +79,8 @@ using namespace tag;
 struct tag_comm_s {
     ncclComm_t nccl = nullptr;   // nullptr when nranks == 1
     int nranks = 1, rank = 0, device = 0;
+    void* devcomm = nullptr;     // ncclDevComm (device API: LSA pointers + barriers), or nullptr
+    bool lsa_all = false;        // every rank is load/store reachable (one NVLink domain)
 };
 
 struct tag_plan_s {
@@ -78,8 +89,16 @@ struct tag_plan_s {
     int64_t K = 0;
     float alpha = 0.f;             // fl32(1/(nB))
     bool use_tc = false;           // tensor-core reconstruction (else SIMT FFMA)
-    void* gx = nullptr;            // gathered X_all  (K x M, wire dtype)
+    void* gx = nullptr;            // gathered X_all  (K x M, wire dtype)   [NCCL gather mode]
     void* gdy = nullptr;           // gathered dY_all (K x N, wire dtype)
+    int gather_mode = TAG_GATHER_NONE;
+    // NVLink push mode: double-buffered [X_all | dY_all] in an NCCL symmetric window
+    void* win_base = nullptr;
+    ncclWindow_t win = nullptr;
+    size_t win_buf_bytes = 0;      // one buffer = K*(M+N)*e_w
+    int parity = 0;
+    void* lx = nullptr;            // local cast scratch for tag_local_grad (B x M, B x N wire)
+    void* ldy = nullptr;
     const void* src_x = nullptr;   // operands of the next reconstruct (set by gather)
     const void* src_dy = nullptr;
     ncclRedOp_t premul{};
@@ -164,6 +183,17 @@ tag_status_t do_gather(tag_plan_s* p, const void* X, const void* dY, cudaStream_
         return TAG_OK;
     }
     const int r = p->comm->rank;
+    if (p->gather_mode == TAG_GATHER_NVLINK_PUSH) {
+        // a1 + a2 fused: cast and store straight into every peer's window (push_gather.cu)
+        const size_t off_x = static_cast<size_t>(p->parity) * p->win_buf_bytes;
+        const size_t off_dy = off_x + static_cast<size_t>(p->K * d.M) * ew;
+        TAG_TRY(launch_push_gather(p->comm->devcomm, p->win, off_x, off_dy, r, X, dY, cx, cy,
+                                   d.in_dtype, d.wire_dtype, PUSH_MAX_CTAS, s));
+        p->src_x = static_cast<char*>(p->win_base) + off_x;
+        p->src_dy = static_cast<char*>(p->win_base) + off_dy;
+        p->parity ^= 1;
+        return TAG_OK;
+    }
     char* gx = static_cast<char*>(p->gx);
     char* gdy = static_cast<char*>(p->gdy);
     const void* sx = X;
@@ -270,6 +300,12 @@ tag_status_t tag_comm_create(const unsigned char id[128], int nranks, int rank, 
             delete c;
             return nccl_fail(r, "ncclCommInitRank");
         }
+        // device API for the NVLink push gather; without it plans use ncclAllGather
+        if (push_devcomm_create(c->nccl, PUSH_MAX_CTAS, &c->devcomm) == TAG_OK)
+            c->lsa_all = push_devcomm_all_lsa(c->devcomm, nranks);
+        else
+            c->devcomm = nullptr;
+        set_error("");
     }
     *out = c;
     return TAG_OK;
@@ -279,6 +315,7 @@ tag_status_t tag_comm_destroy(tag_comm_t c) {
     if (!c) return TAG_OK;
     tag_status_t st = TAG_OK;
     if (c->nccl) {
+        push_devcomm_destroy(c->nccl, c->devcomm);
         ncclResult_t r = ncclCommDestroy(c->nccl);
         if (r != ncclSuccess) st = nccl_fail(r, "ncclCommDestroy");
     }
@@ -308,10 +345,47 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
     auto cleanup = [p]() {
         cudaFree(p->gx);
         cudaFree(p->gdy);
+        cudaFree(p->lx);
+        cudaFree(p->ldy);
+        if (p->win) ncclCommWindowDeregister(p->comm->nccl, p->win);
+        if (p->win_base) ncclMemFree(p->win_base);
         delete p;
     };
-    if (needs_gather_buffers(*d)) {
-        const size_t ew = dtype_size(d->wire_dtype);
+    const size_t ew = dtype_size(d->wire_dtype);
+    if (d->n > 1) {
+        const char* env = std::getenv("TAG_GATHER");
+        const bool want_nccl = env && std::strcmp(env, "nccl") == 0;
+        const bool rows16 = (d->B * d->M * static_cast<int64_t>(ew)) % 16 == 0 &&
+                            (d->B * d->N * static_cast<int64_t>(ew)) % 16 == 0;
+        p->gather_mode = (!want_nccl && c->devcomm && c->lsa_all && rows16) ? TAG_GATHER_NVLINK_PUSH
+                                                                             : TAG_GATHER_NCCL;
+    }
+    if (p->gather_mode == TAG_GATHER_NVLINK_PUSH) {
+        p->win_buf_bytes = static_cast<size_t>(p->K * (d->M + d->N)) * ew;
+        size_t bytes = 2 * p->win_buf_bytes;
+        bytes = (bytes + 4095) & ~static_cast<size_t>(4095);      // NCCL_WIN_REQUIRED_ALIGNMENT
+        ncclResult_t r = ncclMemAlloc(&p->win_base, bytes);
+        if (r == ncclSuccess)
+            r = ncclCommWindowRegister(c->nccl, p->win_base, bytes, &p->win, NCCL_WIN_COLL_SYMMETRIC);
+        if (r != ncclSuccess) {
+            cleanup();
+            return nccl_fail(r, "tag_sfb_plan: symmetric gather window");
+        }
+        // deterministic initial contents (every slot is overwritten by its owner before use)
+        cudaError_t e = cudaMemset(p->win_base, 0, bytes);
+        if (e != cudaSuccess) {
+            cleanup();
+            return cuda_fail(e, "tag_sfb_plan: cudaMemset(window)");
+        }
+        if (d->in_dtype != d->wire_dtype) {
+            e = cudaMalloc(&p->lx, static_cast<size_t>(d->B * d->M) * ew);
+            if (e == cudaSuccess) e = cudaMalloc(&p->ldy, static_cast<size_t>(d->B * d->N) * ew);
+            if (e != cudaSuccess) {
+                cleanup();
+                return cuda_fail(e, "tag_sfb_plan: cudaMalloc(local scratch)");
+            }
+        }
+    } else if (needs_gather_buffers(*d)) {
         cudaError_t e = cudaMalloc(&p->gx, static_cast<size_t>(p->K * d->M) * ew);
         if (e == cudaSuccess) e = cudaMalloc(&p->gdy, static_cast<size_t>(p->K * d->N) * ew);
         if (e != cudaSuccess) {
@@ -339,10 +413,23 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
     return TAG_OK;
 }
 
+tag_status_t tag_sfb_plan_info(tag_sfb_plan_t p, tag_plan_info_t* out) {
+    if (!p || !out) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan_info: NULL argument");
+    out->tensor_cores = p->use_tc ? 1 : 0;
+    out->gather_mode = p->gather_mode;
+    out->K = p->K;
+    out->alpha = p->alpha;
+    return TAG_OK;
+}
+
 tag_status_t tag_sfb_plan_destroy(tag_sfb_plan_t p) {
     if (!p) return TAG_OK;
     set_device(p->comm);
     if (p->has_premul) ncclRedOpDestroy(p->premul, p->comm->nccl);
+    if (p->win) ncclCommWindowDeregister(p->comm->nccl, p->win);
+    if (p->win_base) ncclMemFree(p->win_base);
+    cudaFree(p->lx);
+    cudaFree(p->ldy);
     cudaFree(p->gx);
     cudaFree(p->gdy);
     cudaFree(p->st_x);
@@ -436,8 +523,8 @@ tag_status_t tag_local_grad(tag_sfb_plan_t p, const void* X, const void* dY, voi
         // same operand precision as the SFB path: cast into this rank's gather slot first
         const size_t ew = dtype_size(d.wire_dtype);
         const int r = p->comm->rank;
-        void* lx = static_cast<char*>(p->gx) + r * d.B * d.M * ew;
-        void* ldy = static_cast<char*>(p->gdy) + r * d.B * d.N * ew;
+        void* lx = p->lx ? p->lx : static_cast<char*>(p->gx) + r * d.B * d.M * ew;
+        void* ldy = p->ldy ? p->ldy : static_cast<char*>(p->gdy) + r * d.B * d.N * ew;
         TAG_TRY(launch_pack(X, lx, d.B * d.M, dY, ldy, d.B * d.N, d.in_dtype, d.wire_dtype, s));
         p->src_x = lx;
         p->src_dy = ldy;

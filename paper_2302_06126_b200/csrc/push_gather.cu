@@ -1,0 +1,124 @@
+// push_gather.cu — steps a1 + a2 fused: every replica PUSHES its (cast) sufficient factors
+// straight into the gather buffer of every peer over NVLink 5 / NVSwitch, instead of a pack
+// kernel followed by an NCCL all-gather ("the sufficient factors ... are broadcast to all
+// devices"; D(D-1) transfers of each cut tensor).
+//
+// Mechanism: the gather buffers live in an NCCL symmetric window (ncclMemAlloc +
+// ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC)); the NCCL 2.28 device API gives every GPU
+// load/store-accessible (LSA) pointers into its peers' windows. One kernel per layer:
+//   1. each thread loads 16 output bytes of X_r / dY_r (fp32 -> bf16 RNE cast fused when the
+//      wire dtype differs), and stores them into slot r of every peer's window (peer order
+//      rotated by rank so the n senders spread over the n receivers);
+//   2. an LSA barrier (CTA b of every rank meets CTA b of every peer; release/acquire at system
+//      scope) — when the kernel completes on a rank, every peer's slot has landed there.
+// The window is double-buffered per plan, so the barrier that ends call t also proves every
+// peer has finished reading buffer t-1 (its reconstruction of call t-1 precedes its push of
+// call t in stream order): one barrier per call, none before the stores.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <nccl_device.h>
+
+#include "tag_internal.h"
+
+namespace tag {
+namespace {
+
+constexpr int PUSH_THREADS = 512;
+
+__device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// vx, vy: 16-byte output vectors of this rank's X and dY slots.
+template <bool CAST>
+__global__ void __launch_bounds__(PUSH_THREADS)
+push_gather_kernel(const ncclDevComm comm, ncclWindow_t win, size_t off_x, size_t off_dy,
+                   const void* __restrict__ X, const void* __restrict__ dY, int64_t vx,
+                   int64_t vy, int slot)
+{
+    const int npeers = comm.lsaSize;
+    const int me = comm.lsaRank;
+    const int64_t total = vx + vy;
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t v = tid; v < total; v += nthreads) {
+        const bool isx = v < vx;
+        const int64_t i = isx ? v : v - vx;
+        uint4 val;
+        if constexpr (CAST) {
+            const float4* src = reinterpret_cast<const float4*>(isx ? X : dY) + 2 * i;
+            const float4 a = __ldcs(src);
+            const float4 b = __ldcs(src + 1);
+            val = make_uint4(bf16x2_rn(a.x, a.y), bf16x2_rn(a.z, a.w), bf16x2_rn(b.x, b.y),
+                             bf16x2_rn(b.z, b.w));
+        } else {
+            val = __ldcs(reinterpret_cast<const uint4*>(isx ? X : dY) + i);
+        }
+        const size_t off = isx ? off_x + (static_cast<size_t>(slot) * vx + i) * 16
+                               : off_dy + (static_cast<size_t>(slot) * vy + i) * 16;
+        for (int k = 0; k < npeers; ++k) {
+            const int p = (me + k) % npeers;
+            *reinterpret_cast<uint4*>(ncclGetLsaPointer(win, off, p)) = val;
+        }
+    }
+    // all of this CTA's stores are released to every peer; CTA b waits for CTA b everywhere
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
+}  // namespace
+
+tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, void** out) {
+    ncclDevCommRequirements reqs;
+    std::memset(&reqs, 0, sizeof reqs);
+    reqs.lsaBarrierCount = max_ctas;
+    ncclDevComm* dc = new ncclDevComm;
+    ncclResult_t r = ncclDevCommCreate(comm, &reqs, dc);
+    if (r != ncclSuccess) {
+        delete dc;
+        return fail(TAG_ERR_NCCL, std::string("ncclDevCommCreate: ") + ncclGetErrorString(r));
+    }
+    *out = dc;
+    return TAG_OK;
+}
+
+void push_devcomm_destroy(ncclComm_t comm, void* dc) {
+    if (!dc) return;
+    ncclDevCommDestroy(comm, static_cast<ncclDevComm*>(dc));
+    delete static_cast<ncclDevComm*>(dc);
+}
+
+bool push_devcomm_all_lsa(const void* dc, int nranks) {
+    const ncclDevComm* d = static_cast<const ncclDevComm*>(dc);
+    return d && d->lsaSize == nranks && d->nRanks == nranks;
+}
+
+int push_grid(int64_t vectors, int max_ctas) {
+    int64_t g = (vectors + PUSH_THREADS - 1) / PUSH_THREADS;
+    if (g > max_ctas) g = max_ctas;
+    if (g > num_sms()) g = num_sms();
+    return g < 1 ? 1 : static_cast<int>(g);
+}
+
+tag_status_t launch_push_gather(const void* dc, ncclWindow_t win, size_t off_x, size_t off_dy,
+                                int slot, const void* X, const void* dY, int64_t cx, int64_t cy,
+                                tag_dtype_t in, tag_dtype_t wire, int max_ctas, cudaStream_t s) {
+    const ncclDevComm& comm = *static_cast<const ncclDevComm*>(dc);
+    const int64_t ew = static_cast<int64_t>(dtype_size(wire));
+    const int64_t vx = cx * ew / 16, vy = cy * ew / 16;
+    const int grid = push_grid(vx + vy, max_ctas);
+    if (in == wire)
+        push_gather_kernel<false><<<grid, PUSH_THREADS, 0, s>>>(comm, win, off_x, off_dy, X, dY,
+                                                                 vx, vy, slot);
+    else
+        push_gather_kernel<true><<<grid, PUSH_THREADS, 0, s>>>(comm, win, off_x, off_dy, X, dY,
+                                                                vx, vy, slot);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "launch push_gather_kernel");
+    count_launch();
+    return TAG_OK;
+}
+
+}  // namespace tag

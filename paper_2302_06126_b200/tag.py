@@ -36,6 +36,15 @@ class SfbDesc(ctypes.Structure):
                 ("momentum", ctypes.c_float), ("weight_decay", ctypes.c_float)]
 
 
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("tensor_cores", ctypes.c_int), ("gather_mode", ctypes.c_int),
+                ("K", ctypes.c_int64), ("alpha", ctypes.c_float)]
+
+
+GATHER_NONE, GATHER_NCCL, GATHER_NVLINK_PUSH = 0, 1, 2
+GATHER_NAMES = {0: "none", 1: "nccl_allgather", 2: "nvlink_push"}
+
+
 class LayerDesc(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int64), ("N", ctypes.c_int64), ("B", ctypes.c_int64),
                 ("factor_dtype", ctypes.c_int), ("grad_dtype", ctypes.c_int)]
@@ -58,6 +67,7 @@ _SIGS = {
     "tag_comm_info": ([_vp, _p(_i), _p(_i), _p(_i)], _st),
     "tag_sfb_plan": ([_vp, _p(SfbDesc), _p(_vp)], _st),
     "tag_sfb_plan_destroy": ([_vp], _st),
+    "tag_sfb_plan_info": ([_vp, _p(PlanInfo)], _st),
     "tag_sfb_sync": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_gather": ([_vp, _vp, _vp, _vp], _st),
     "tag_sfb_reconstruct": ([_vp, _vp, _vp], _st),
@@ -166,6 +176,12 @@ class SfbPlan:
         h = _vp()
         _check(_lib.tag_sfb_plan(comm.handle, ctypes.byref(d), ctypes.byref(h)), "tag_sfb_plan")
         self._h = h
+
+    def info(self):
+        i = PlanInfo()
+        _check(_lib.tag_sfb_plan_info(self._h, ctypes.byref(i)), "tag_sfb_plan_info")
+        return {"tensor_cores": bool(i.tensor_cores), "gather": GATHER_NAMES[i.gather_mode],
+                "K": int(i.K), "alpha": float(i.alpha)}
 
     # dtypes as torch dtypes
     @property

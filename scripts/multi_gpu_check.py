@@ -1,0 +1,138 @@
+#!/usr/bin/env python3
+"""Multi-GPU parity of the SFB path through the C ABI (run under torchrun, one process per GPU).
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port P scripts/multi_gpu_check.py
+
+Checks, for n = world size ("MatMul ops on each device can reconstruct identical
+gradients"):
+  1. dW is bitwise identical on every rank (hash all-gathered over torch.distributed);
+  2. integer inputs: dW equals fl32(S * fl32(1/(nB))) bit for bit (S from the oracle);
+  3. random VGG-shaped inputs: rel. Frobenius <= 1e-5 vs the oracle on the exact bf16 values;
+  4. the dense baseline (local GEMM + AllReduce with PreMulSum 1/(nB)) agrees with SFB;
+  5. fp32 toy config (64x32, B=4) <= 1e-5; fp32 -> bf16 wire (pack + in-place gather);
+  6. fused SGD-momentum: identical W, v on every rank and equal to the unfused path;
+  7. selector decisions identical on every rank and equal to the oracle's.
+Rank 0 prints one JSON line with the results; exit code 0 iff every check passed.
+"""
+import hashlib
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402  (test infrastructure)
+from paper_2302_06126_b200 import dist as tdist  # noqa: E402
+from paper_2302_06126_b200 import synth, tag  # noqa: E402
+
+TDT = {"f32": torch.float32, "bf16": torch.bfloat16}
+
+
+def digest(t):
+    return hashlib.sha256(t.contiguous().view(torch.uint8).cpu().numpy().tobytes()).hexdigest()
+
+
+def rel_fro(a, r):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - r) / max(np.linalg.norm(r), 1e-300))
+
+
+def main():
+    rank, local_rank, world = tdist.init_from_env()
+    torch.cuda.set_device(local_rank)
+    comm = tdist.bootstrap_comm(tag, local_rank)
+    n = world
+    results = {}
+    modes = set()
+    ok = True
+
+    def record(name, passed, **info):
+        nonlocal ok
+        ok = ok and bool(passed)
+        results[name] = dict(passed=bool(passed), **info)
+
+    def run(cid, li, M, N, B, xd, dyd, in_dt, wire_dt, out_dt):
+        X, dY = synth.factors(cid, li, rank, M, N, B, xd, dyd)
+        plan = tag.SfbPlan(comm, M, N, B, in_dt, wire_dt, out_dt)
+        modes.add(plan.info()["gather"])
+        Xd = torch.from_numpy(X).to(TDT[in_dt]).cuda()
+        dYd = torch.from_numpy(dY).to(TDT[in_dt]).cuda()
+        dW = torch.full((M, N), float("nan"), dtype=TDT[out_dt], device="cuda")
+        for _ in range(3):                   # exercises both halves of a double-buffered window
+            plan.sync(Xd, dYd, dW)
+        dense = torch.empty_like(dW)
+        plan.local_grad(Xd, dYd, dense)
+        plan.dense_allreduce(dense)
+        torch.cuda.synchronize()
+        hashes = tdist.all_gather_object(digest(dW))
+        plan.close()
+        Xall, dYall = synth.all_factors(cid, li, n, M, N, B, xd, dyd)
+        wire = TDT[wire_dt]
+        Xe = torch.from_numpy(Xall).to(wire).double().numpy()
+        dYe = torch.from_numpy(dYall).to(wire).double().numpy()
+        return dW, dense, hashes, Xall, dYall, Xe, dYe
+
+    # 1-4: VGG-19 fc7 / fc8 shapes, B = 32 per GPU, bf16
+    for li, (M, N, dyd) in [(7, (4096, 4096, "masked_small")), (8, (4096, 1000, "softmax_onehot"))]:
+        dW, dense, hashes, Xall, dYall, Xe, dYe = run(2, li, M, N, 32, "relu", dyd, "bf16", "bf16", "f32")
+        ref = oracle.sfb_dw(Xe, dYe)
+        e = rel_fro(dW.cpu().numpy(), ref)
+        ed = rel_fro(dense.cpu().numpy(), ref)
+        record(f"vgg_{M}x{N}", len(set(hashes)) == 1 and e <= 1e-5 and ed <= 1e-5,
+               rel_fro=e, dense_rel_fro=ed, identical_ranks=len(set(hashes)) == 1)
+
+    # 2: integer inputs, bit exact (odd tile edges: 520 x 264)
+    dW, dense, hashes, Xall, dYall, Xe, dYe = run(60, 0, 520, 264, 24, "int3", "int3", "bf16", "bf16", "f32")
+    S = oracle.sfb_sum(Xall, dYall)
+    want = S.astype(np.float32) * np.float32(1.0 / (n * 24))
+    got = dW.cpu().numpy()
+    record("int_bit_exact", np.array_equal(got.view(np.uint32), want.view(np.uint32))
+           and len(set(hashes)) == 1, max_abs=float(np.abs(got - want).max()))
+
+    # 5: fp32 toy (config 1) and fp32 -> bf16 wire with a bf16 dW
+    dW, dense, hashes, Xall, dYall, Xe, dYe = run(1, 0, 64, 32, 4, "normal", "normal", "f32", "f32", "f32")
+    e = rel_fro(dW.cpu().numpy(), oracle.sfb_dw(Xall, dYall))
+    record("toy_fp32", e <= 1e-5 and len(set(hashes)) == 1, rel_fro=e)
+    dW, dense, hashes, Xall, dYall, Xe, dYe = run(4, 1, 512, 2048, 256, "normal", "small", "f32", "bf16", "bf16")
+    e = rel_fro(dW.float().cpu().numpy(), oracle.sfb_dw(Xe, dYe))
+    record("f32_in_bf16_wire_bf16_out", e <= 8e-3 and len(set(hashes)) == 1, rel_fro=e)
+
+    # 6: fused SGD (BERT-L pooler shape, B = 2 per GPU)
+    M, N, B = 1024, 1024, 2
+    X, dY = synth.factors(5, 3, rank, M, N, B, "tanh", "small")
+    W0, v0 = synth.sgd_state(5, 3, M, N)
+    plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", fuse_sgd=True, lr=1e-3, momentum=0.9)
+    Xd, dYd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(dY).to(torch.bfloat16).cuda()
+    W1, v1 = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
+    for _ in range(3):
+        plan.sync_sgd(Xd, dYd, W1, v1, None)
+    W2, v2 = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
+    dW2 = torch.empty(M, N, device="cuda")
+    for _ in range(3):
+        plan.sync(Xd, dYd, dW2)
+        plan.sgd_step(dW2, W2, v2)
+    torch.cuda.synchronize()
+    hashes = tdist.all_gather_object(digest(W1) + digest(v1))
+    record("fused_sgd", torch.equal(W1, W2) and torch.equal(v1, v2) and len(set(hashes)) == 1)
+    plan.close()
+
+    # 7: selector identical on all ranks and equal to the oracle
+    lays = [dict(M=L.M, N=L.N, B=L.B) for c in (2, 3, 4, 5) for L in synth.CONFIGS[c].layers]
+    got = tag.select([dict(l, factor_dtype="bf16", grad_dtype="f32") for l in lays], n,
+                     900_000_000_000, 1421400000000000)
+    want = [oracle.selector.select(dict(l, e_w=2, e_g=4), dict(n=n, tau=900_000_000_000,
+                                                                F=1421400000000000)) for l in lays]
+    allg = tdist.all_gather_object(got)
+    record("selector", got == want and all(g == got for g in allg))
+
+    comm.close()
+    ok_all = all(tdist.all_gather_object(ok))
+    if rank == 0:
+        print(json.dumps({"n": n, "ok": ok_all, "gather_modes": sorted(modes), "results": results}),
+              flush=True)
+    sys.exit(0 if ok_all else 1)
+
+
+if __name__ == "__main__":
+    main()

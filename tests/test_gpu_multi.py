@@ -1,0 +1,41 @@
+"""Multi-GPU parity (n = 2 and 4) through torchrun + NCCL; skipped when the box has one GPU
+(the single-GPU virtual-n tests in test_gpu_recon.py cover the n-replica reconstruction)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("gather", ["push", "nccl"])
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_multi_gpu_sfb(cuda, nproc, gather):
+    if torch.cuda.device_count() < nproc:
+        pytest.skip(f"needs {nproc} GPUs, box has {torch.cuda.device_count()}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           os.path.join(ROOT, "scripts", "multi_gpu_check.py")]
+    env = dict(os.environ)
+    if gather == "nccl":
+        env["TAG_GATHER"] = "nccl"
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(lines[-1])
+    assert res["ok"] and res["n"] == nproc, res
+    want = "nccl_allgather" if gather == "nccl" else "nvlink_push"
+    assert want in res["gather_modes"], res
