@@ -166,6 +166,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--ref-mac", type=float, default=2.5e10)
+    ap.add_argument("--per-layer-step", action="store_true",
+                    help="time the step as one tag_sfb_sync per layer instead of one bucket")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "need >= 3 warm-up steps"
 
@@ -203,39 +205,62 @@ def main():
         flush_rd.sum()
     nl = len(layers)
 
-    def step(evs=None):
+    Xs, dYs, dWs = [l["X"] for l in layers], [l["dY"] for l in layers], [l["dW"] for l in layers]
+    # the step is one bucket: one push kernel (n > 1) + one persistent reconstruction launch
+    group = None if args.per_layer_step else tag.SfbGroup([l["plan"] for l in layers])
+
+    def step(ev_mid=None):
         with torch.cuda.stream(stream):
-            for i, l in enumerate(layers):
-                if evs is None:
+            if group is not None:
+                group.gather(Xs, dYs, stream)
+                if ev_mid is not None:
+                    ev_mid.record(stream)
+                group.reconstruct(dWs, stream)
+            else:
+                for l in layers:
                     l["plan"].sync(l["X"], l["dY"], l["dW"], stream)
-                else:
+
+    def start_events(k):
+        flush_l2()
+        torch.cuda.synchronize()
+        tdist.barrier()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
+        with torch.cuda.stream(stream):
+            # a ~40 us device spin ahead of the start event lets the host enqueue the whole step,
+            # so the interval measures device time, not Python launch latency
+            torch.cuda._sleep(SPIN_CYCLES)
+        evs[0].record(stream)
+        return evs
+
+    def timed_steps(nsteps):
+        """Whole steps: [start, after gather (group mode), end] per step."""
+        step_ms, recon_ms = [], []
+        for _ in range(nsteps):
+            evs = start_events(3)
+            step(evs[1] if group is not None else None)
+            evs[2].record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(evs[0].elapsed_time(evs[2]))
+            if group is not None:
+                recon_ms.append(evs[1].elapsed_time(evs[2]))
+        return step_ms, recon_ms
+
+    def timed_layers(nsteps):
+        """Per-layer staged pass: gather | reconstruct of each layer on its own."""
+        rec, syn = [[] for _ in range(nl)], [[] for _ in range(nl)]
+        for _ in range(nsteps):
+            evs = start_events(2 * nl + 1)
+            with torch.cuda.stream(stream):
+                for i, l in enumerate(layers):
                     l["plan"].gather(l["X"], l["dY"], stream)
                     evs[2 * i + 1].record(stream)
                     l["plan"].reconstruct(l["dW"], stream)
                     evs[2 * i + 2].record(stream)
-
-    def timed_loop(nsteps, staged):
-        per_step, per_layer_recon, per_layer_sync = [], [[] for _ in range(nl)], [[] for _ in range(nl)]
-        for _ in range(nsteps):
-            flush_l2()
             torch.cuda.synchronize()
-            tdist.barrier()
-            evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * nl + 1)]
-            with torch.cuda.stream(stream):
-                # a ~40 us spin ahead of the start event lets the host enqueue the whole step, so
-                # the interval measures device time, not Python launch latency
-                torch.cuda._sleep(SPIN_CYCLES)
-            evs[0].record(stream)
-            step(evs if staged else None)
-            if not staged:
-                evs[-1].record(stream)
-            torch.cuda.synchronize()
-            per_step.append(evs[0].elapsed_time(evs[-1 if not staged else 2 * nl]))
-            if staged:
-                for i in range(nl):
-                    per_layer_recon[i].append(evs[2 * i + 1].elapsed_time(evs[2 * i + 2]))
-                    per_layer_sync[i].append(evs[2 * i].elapsed_time(evs[2 * i + 2]))
-        return per_step, per_layer_recon, per_layer_sync
+            for i in range(nl):
+                rec[i].append(evs[2 * i + 1].elapsed_time(evs[2 * i + 2]))
+                syn[i].append(evs[2 * i].elapsed_time(evs[2 * i + 2]))
+        return rec, syn
 
     # ---------------------------------------------------------------- warm-up + timed region
     for _ in range(args.warmup):
@@ -244,21 +269,25 @@ def main():
     tdist.barrier()
     launches0 = tag.kernel_launches()
     with ClockSampler(local_rank) as clk:
-        steps_ms, recon_ms, sync_ms = timed_loop(args.steps, staged=True)
+        steps_ms, recon_ms = timed_steps(args.steps)
     launches = tag.kernel_launches() - launches0
     torch.cuda.synchronize()
     tdist.barrier()
+    layer_recon_ms, layer_sync_ms = timed_layers(max(5, min(args.steps, 30)))
 
-    mean_step = statistics.mean(steps_ms)
-    t_step_ms = tdist.max_over_ranks(mean_step)
+    t_step_ms = tdist.max_over_ranks(statistics.mean(steps_ms))
     dw_bytes = sum(l["L"].M * l["L"].N * ESIZE[cfg.out_dtype] for l in layers)
     value = n * dw_bytes / (t_step_ms * 1e-3) / 1e9
 
-    # roofline of the dominant kernel: the reconstruction (recon_tc_kernel), HBM-bound here
+    # roofline of the dominant kernel: the (grouped) reconstruction, HBM-bound at these shapes
     alg_bytes = sum(n * l["L"].B * (l["L"].M + l["L"].N) * ESIZE[cfg.wire_dtype]
                     + l["L"].M * l["L"].N * ESIZE[cfg.out_dtype] for l in layers)
-    recon_mean_ms = [statistics.mean(r) for r in recon_ms]
-    recon_total_ms = tdist.max_over_ranks(sum(recon_mean_ms))
+    if group is not None:
+        recon_total_ms = tdist.max_over_ranks(statistics.mean(recon_ms))
+        launches_per_step = 1
+    else:
+        recon_total_ms = tdist.max_over_ranks(sum(statistics.mean(r) for r in layer_recon_ms))
+        launches_per_step = nl
     achieved = alg_bytes / (recon_total_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "recon_traffic.json")
@@ -267,18 +296,19 @@ def main():
             traffic = json.load(open(tp)).get(f"config{args.config}_n{n}")
         except Exception:
             traffic = None
-    roofline = {"kernel": "recon_tc_kernel (tcgen05 reconstruction + fused 1/(nB) epilogue)",
+    roofline = {"kernel": "recon_tc_kernel (grouped tcgen05 reconstruction, fused 1/(nB) epilogue)",
                 "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
                 "traffic": traffic, "peak_source": peak_src,
-                "algorithmic_bytes_per_step": alg_bytes,
-                "recon_share_of_step": round(recon_total_ms / t_step_ms, 3)}
+                "algorithmic_bytes_per_step": alg_bytes, "launches_per_step": launches_per_step,
+                "kernel_us": round(recon_total_ms * 1e3, 2),
+                "share_of_step": round(recon_total_ms / t_step_ms, 3)}
 
     per_layer = {}
     for i, l in enumerate(layers):
         L = l["L"]
-        t_sync = tdist.max_over_ranks(statistics.median(sync_ms[i]))
-        t_rec = tdist.max_over_ranks(statistics.median(recon_ms[i]))
+        t_sync = tdist.max_over_ranks(statistics.median(layer_sync_ms[i]))
+        t_rec = tdist.max_over_ranks(statistics.median(layer_recon_ms[i]))
         flops = 2.0 * L.M * L.N * n * L.B
         rbytes = n * L.B * (L.M + L.N) * ESIZE[cfg.wire_dtype] + L.M * L.N * ESIZE[cfg.out_dtype]
         ag = (n - 1) * L.B * (L.M + L.N) * ESIZE[cfg.wire_dtype]
@@ -291,6 +321,14 @@ def main():
             "allgather_busbw_GBps": round(ag / ((t_sync - t_rec) * 1e-3) / 1e9, 1) if n > 1 else None,
             "selector": {0: "allreduce", 1: "sfb", 2: "none"}[choices[i]],
             "gather": l["plan"].info()["gather"]}
+    if group is not None and n > 1:
+        t_gather = tdist.max_over_ranks(statistics.mean(
+            [s_ - r_ for s_, r_ in zip(steps_ms, recon_ms)]))
+        ag_all = sum((n - 1) * l["L"].B * (l["L"].M + l["L"].N) * ESIZE[cfg.wire_dtype] for l in layers)
+        per_layer["bucket_gather"] = {"us": round(t_gather * 1e3, 2),
+                                      "ingress_MB": round(ag_all / 1e6, 3),
+                                      "busbw_GBps": round(ag_all / (t_gather * 1e-3) / 1e9, 1),
+                                      "frac_of_900": round(ag_all / (t_gather * 1e-3) / 900e9, 4)}
 
     # ---------------------------------------------------------------- dense baseline (n > 1)
     if n > 1 and not args.no_dense:
@@ -355,6 +393,8 @@ def main():
                 "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
                 "lib": tag.version()}
         print(json.dumps(line), flush=True)
+    if group is not None:
+        group.close()
     for l in layers:
         l["plan"].close()
     comm.close()

@@ -172,6 +172,28 @@ tag_status_t tag_sfb_sync_host(tag_sfb_plan_t plan, const void* X_host, const vo
                                void* dW_host, tag_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------ */
+/* Buckets: several layers synchronised together                                             */
+/* ------------------------------------------------------------------------------------------ */
+/* A group (bucket) of 1..8 plans of the same comm and the same in/wire/out dtypes, without
+ * fuse_sgd. tag_sfb_group_sync runs steps a1-a4 of every layer with ONE push kernel (one LSA
+ * barrier; or one grouped NCCL call) and ONE persistent tensor-core launch over all layers' output
+ * tiles, so launch latency, pipeline ramp-up, the last partial wave and the barrier latency are
+ * paid once per bucket instead of once per layer. Results are bitwise identical to calling
+ * tag_sfb_sync on each plan. The group borrows the plans (destroy the group first). Creating a
+ * group is host-only; using it is COLLECTIVE: every rank must build the same groups in the same
+ * plan order. X[i], dY[i], dW[i] are the arguments tag_sfb_sync would take for plans[i]. */
+typedef struct tag_group_s* tag_sfb_group_t;
+tag_status_t tag_sfb_group_create(const tag_sfb_plan_t* plans, int count, tag_sfb_group_t* out);
+tag_status_t tag_sfb_group_destroy(tag_sfb_group_t group);
+tag_status_t tag_sfb_group_sync(tag_sfb_group_t group, const void* const* X,
+                                const void* const* dY, void* const* dW, tag_stream_t stream);
+/* Stage split, as for single plans: gather = a1 + a2 of every layer, reconstruct = a3 + a4. */
+tag_status_t tag_sfb_group_gather(tag_sfb_group_t group, const void* const* X,
+                                  const void* const* dY, tag_stream_t stream);
+tag_status_t tag_sfb_group_reconstruct(tag_sfb_group_t group, void* const* dW,
+                                       tag_stream_t stream);
+
+/* ------------------------------------------------------------------------------------------ */
 /* Dense-gradient baseline ("Replicate with AllReduce")                 */
 /* ------------------------------------------------------------------------------------------ */
 /* Local, unscaled gradient of this replica: dW_local = X_r^T dY_r (K = B) in out_dtype, operands

@@ -11,6 +11,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "tag_internal.h"
 
@@ -19,9 +20,6 @@ namespace tag {
 tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, void** out);
 void push_devcomm_destroy(ncclComm_t comm, void* dc);
 bool push_devcomm_all_lsa(const void* dc, int nranks);
-tag_status_t launch_push_gather(const void* dc, ncclWindow_t win, size_t off_x, size_t off_dy,
-                                int slot, const void* X, const void* dY, int64_t cx, int64_t cy,
-                                tag_dtype_t in, tag_dtype_t wire, int max_ctas, cudaStream_t s);
 constexpr int PUSH_MAX_CTAS = 148;
 
 std::atomic<uint64_t> g_launches{0};
@@ -109,6 +107,12 @@ struct tag_plan_s {
     void* st_dw = nullptr;
 };
 
+struct tag_group_s {
+    std::vector<tag_plan_s*> plans;
+    bool push_all = false;     // every plan gathers by NVLink push -> one grouped push kernel
+    bool tc_all = false;       // every plan reconstructs on the tensor cores -> one launch
+};
+
 namespace {
 
 ncclDataType_t nccl_type(tag_dtype_t t) { return t == TAG_F32 ? ncclFloat32 : ncclBfloat16; }
@@ -187,8 +191,9 @@ tag_status_t do_gather(tag_plan_s* p, const void* X, const void* dY, cudaStream_
         // a1 + a2 fused: cast and store straight into every peer's window (push_gather.cu)
         const size_t off_x = static_cast<size_t>(p->parity) * p->win_buf_bytes;
         const size_t off_dy = off_x + static_cast<size_t>(p->K * d.M) * ew;
-        TAG_TRY(launch_push_gather(p->comm->devcomm, p->win, off_x, off_dy, r, X, dY, cx, cy,
-                                   d.in_dtype, d.wire_dtype, PUSH_MAX_CTAS, s));
+        PushSegment seg{X, dY, p->win, off_x, off_dy, cx, cy};
+        TAG_TRY(launch_push_gather_group(p->comm->devcomm, &seg, 1, r, d.in_dtype, d.wire_dtype,
+                                         PUSH_MAX_CTAS, s));
         p->src_x = static_cast<char*>(p->win_base) + off_x;
         p->src_dy = static_cast<char*>(p->win_base) + off_dy;
         p->parity ^= 1;
@@ -568,6 +573,124 @@ tag_status_t tag_sgd_step(tag_sfb_plan_t p, const float* dW, float* W, float* v,
     TAG_TRY(set_device(p->comm));
     return launch_sgd(dW, W, v, p->d.M * p->d.N, p->d.lr, p->d.momentum, p->d.weight_decay,
                       reinterpret_cast<cudaStream_t>(stream));
+}
+
+tag_status_t tag_sfb_group_create(const tag_sfb_plan_t* plans, int count, tag_sfb_group_t* out) {
+    if (!plans || !out) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_create: NULL argument");
+    if (count < 1 || count > MAX_GROUP)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_create: count must be in [1, 8]");
+    for (int i = 0; i < count; ++i) {
+        const tag_plan_s* p = plans[i];
+        if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_create: NULL plan");
+        if (p->comm != plans[0]->comm || p->d.in_dtype != plans[0]->d.in_dtype ||
+            p->d.wire_dtype != plans[0]->d.wire_dtype || p->d.out_dtype != plans[0]->d.out_dtype)
+            return fail(TAG_ERR_INVALID_ARG,
+                        "tag_sfb_group_create: plans must share the comm and the dtypes");
+        if (p->d.fuse_sgd)
+            return fail(TAG_ERR_UNSUPPORTED, "tag_sfb_group_create: fuse_sgd plans are not groupable");
+        for (int j = 0; j < i; ++j)
+            if (plans[j] == p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_create: duplicate plan");
+    }
+    tag_group_s* g = new tag_group_s;
+    g->plans.assign(plans, plans + count);
+    g->push_all = true;
+    g->tc_all = true;
+    for (tag_plan_s* p : g->plans) {
+        g->push_all = g->push_all && p->gather_mode == TAG_GATHER_NVLINK_PUSH;
+        g->tc_all = g->tc_all && p->use_tc;
+    }
+    *out = g;
+    return TAG_OK;
+}
+
+tag_status_t tag_sfb_group_destroy(tag_sfb_group_t g) {
+    delete g;
+    return TAG_OK;
+}
+
+tag_status_t tag_sfb_group_gather(tag_sfb_group_t g, const void* const* X, const void* const* dY,
+                                  tag_stream_t stream) {
+    if (!g || !X || !dY) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_gather: NULL argument");
+    const int count = static_cast<int>(g->plans.size());
+    for (int i = 0; i < count; ++i) TAG_TRY(check_ptrs("tag_sfb_group_gather", {X[i], dY[i]}));
+    tag_comm_s* c = g->plans[0]->comm;
+    TAG_TRY(set_device(c));
+    TAG_TRY(check_async(c));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (g->push_all) {
+        PushSegment seg[MAX_GROUP];
+        for (int i = 0; i < count; ++i) {
+            tag_plan_s* p = g->plans[i];
+            const size_t ew = dtype_size(p->d.wire_dtype);
+            const size_t off_x = static_cast<size_t>(p->parity) * p->win_buf_bytes;
+            const size_t off_dy = off_x + static_cast<size_t>(p->K * p->d.M) * ew;
+            seg[i] = PushSegment{X[i], dY[i], p->win, off_x, off_dy, p->d.B * p->d.M, p->d.B * p->d.N};
+        }
+        tag_plan_s* p0 = g->plans[0];
+        TAG_TRY(launch_push_gather_group(c->devcomm, seg, count, c->rank, p0->d.in_dtype,
+                                         p0->d.wire_dtype, PUSH_MAX_CTAS, s));
+        for (int i = 0; i < count; ++i) {
+            tag_plan_s* p = g->plans[i];
+            p->src_x = static_cast<char*>(p->win_base) + seg[i].off_x;
+            p->src_dy = static_cast<char*>(p->win_base) + seg[i].off_dy;
+            p->parity ^= 1;
+        }
+        return TAG_OK;
+    }
+    // mixed / NCCL mode: one NCCL group around every plan's gather (nested groups are legal)
+    const bool nccl = c->nccl != nullptr;
+    if (nccl) {
+        ncclResult_t r = ncclGroupStart();
+        if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+    }
+    tag_status_t st = TAG_OK;
+    for (int i = 0; i < count && st == TAG_OK; ++i) st = do_gather(g->plans[i], X[i], dY[i], s);
+    if (nccl) {
+        ncclResult_t r = ncclGroupEnd();
+        if (st == TAG_OK && r != ncclSuccess) return nccl_fail(r, "ncclGroupEnd");
+    }
+    return st;
+}
+
+tag_status_t tag_sfb_group_reconstruct(tag_sfb_group_t g, void* const* dW, tag_stream_t stream) {
+    if (!g || !dW) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_reconstruct: NULL argument");
+    const int count = static_cast<int>(g->plans.size());
+    for (int i = 0; i < count; ++i) {
+        TAG_TRY(check_ptrs("tag_sfb_group_reconstruct", {dW[i]}));
+        if (!g->plans[i]->src_x)
+            return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_reconstruct: no factors gathered yet");
+    }
+    TAG_TRY(set_device(g->plans[0]->comm));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    ReconArgs a[MAX_GROUP];
+    bool tc = g->tc_all;
+    for (int i = 0; i < count; ++i) {
+        tag_plan_s* p = g->plans[i];
+        a[i] = ReconArgs{};
+        a[i].A = p->src_x;
+        a[i].Bm = p->src_dy;
+        a[i].C = dW[i];
+        a[i].M = p->d.M;
+        a[i].N = p->d.N;
+        a[i].K = p->K;
+        a[i].wire = p->d.wire_dtype;
+        a[i].out = p->d.out_dtype;
+        a[i].alpha = p->alpha;
+        tc = tc && recon_tc_ok(a[i]);
+    }
+    if (tc) return launch_recon_tc_group(a, count, s);
+    for (int i = 0; i < count; ++i)
+        TAG_TRY(do_recon(g->plans[i], dW[i], false, nullptr, nullptr, g->plans[i]->K,
+                         g->plans[i]->alpha, s));
+    return TAG_OK;
+}
+
+tag_status_t tag_sfb_group_sync(tag_sfb_group_t g, const void* const* X, const void* const* dY,
+                                void* const* dW, tag_stream_t stream) {
+    if (!g || !X || !dY || !dW) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync: NULL argument");
+    for (size_t i = 0; i < g->plans.size(); ++i) TAG_TRY(check_ptrs("tag_sfb_group_sync", {dW[i]}));
+    TAG_TRY(tag_sfb_group_gather(g, X, dY, stream));
+    return tag_sfb_group_reconstruct(g, dW, stream);
 }
 
 }  // extern "C"

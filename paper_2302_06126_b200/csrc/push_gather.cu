@@ -5,7 +5,8 @@
 //
 // Mechanism: the gather buffers live in an NCCL symmetric window (ncclMemAlloc +
 // ncclCommWindowRegister(NCCL_WIN_COLL_SYMMETRIC)); the NCCL 2.28 device API gives every GPU
-// load/store-accessible (LSA) pointers into its peers' windows. One kernel per layer:
+// load/store-accessible (LSA) pointers into its peers' windows. One kernel per layer, or per
+// bucket of layers (tag_sfb_group_*):
 //   1. each thread loads 16 output bytes of X_r / dY_r (fp32 -> bf16 RNE cast fused when the
 //      wire dtype differs), and stores them into slot r of every peer's window (peer order
 //      rotated by rank so the n senders spread over the n receivers);
@@ -19,6 +20,8 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <cstring>
+
 #include "tag_internal.h"
 
 namespace tag {
@@ -31,36 +34,54 @@ __device__ __forceinline__ uint32_t bf16x2_rn(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// vx, vy: 16-byte output vectors of this rank's X and dY slots.
+// One push kernel serves a whole bucket of layers: segment i covers layer i's X slot then its
+// dY slot (16-byte output vectors); one LSA barrier per CTA at the end covers all of them.
+struct PushLayer {
+    const void* X;
+    const void* dY;
+    ncclWindow_t win;
+    size_t off_x, off_dy;   // byte offsets of X_all / dY_all of the current buffer in `win`
+    int64_t vx, vy;         // 16-byte output vectors of this rank's X_r / dY_r
+    int64_t vbegin;         // first global vector index of this layer
+};
+
+struct PushGroup {
+    PushLayer L[MAX_GROUP];
+    int count;
+    int64_t total;
+    int slot;               // this rank's slot (world rank)
+};
+
 template <bool CAST>
 __global__ void __launch_bounds__(PUSH_THREADS)
-push_gather_kernel(const ncclDevComm comm, ncclWindow_t win, size_t off_x, size_t off_dy,
-                   const void* __restrict__ X, const void* __restrict__ dY, int64_t vx,
-                   int64_t vy, int slot)
+push_gather_kernel(const ncclDevComm comm, const __grid_constant__ PushGroup g)
 {
     const int npeers = comm.lsaSize;
     const int me = comm.lsaRank;
-    const int64_t total = vx + vy;
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    for (int64_t v = tid; v < total; v += nthreads) {
-        const bool isx = v < vx;
-        const int64_t i = isx ? v : v - vx;
+    int li = 0;
+    for (int64_t v = tid; v < g.total; v += nthreads) {
+        while (li + 1 < g.count && v >= g.L[li + 1].vbegin) ++li;   // v only grows
+        const PushLayer& L = g.L[li];
+        const int64_t lv = v - L.vbegin;
+        const bool isx = lv < L.vx;
+        const int64_t i = isx ? lv : lv - L.vx;
         uint4 val;
         if constexpr (CAST) {
-            const float4* src = reinterpret_cast<const float4*>(isx ? X : dY) + 2 * i;
+            const float4* src = reinterpret_cast<const float4*>(isx ? L.X : L.dY) + 2 * i;
             const float4 a = __ldcs(src);
             const float4 b = __ldcs(src + 1);
             val = make_uint4(bf16x2_rn(a.x, a.y), bf16x2_rn(a.z, a.w), bf16x2_rn(b.x, b.y),
                              bf16x2_rn(b.z, b.w));
         } else {
-            val = __ldcs(reinterpret_cast<const uint4*>(isx ? X : dY) + i);
+            val = __ldcs(reinterpret_cast<const uint4*>(isx ? L.X : L.dY) + i);
         }
-        const size_t off = isx ? off_x + (static_cast<size_t>(slot) * vx + i) * 16
-                               : off_dy + (static_cast<size_t>(slot) * vy + i) * 16;
+        const size_t off = isx ? L.off_x + (static_cast<size_t>(g.slot) * L.vx + i) * 16
+                               : L.off_dy + (static_cast<size_t>(g.slot) * L.vy + i) * 16;
         for (int k = 0; k < npeers; ++k) {
-            const int p = (me + k) % npeers;
-            *reinterpret_cast<uint4*>(ncclGetLsaPointer(win, off, p)) = val;
+            const int p = (me + k) % npeers;   // rotate so the senders spread over receivers
+            *reinterpret_cast<uint4*>(ncclGetLsaPointer(L.win, off, p)) = val;
         }
     }
     // all of this CTA's stores are released to every peer; CTA b waits for CTA b everywhere
@@ -102,19 +123,35 @@ int push_grid(int64_t vectors, int max_ctas) {
     return g < 1 ? 1 : static_cast<int>(g);
 }
 
-tag_status_t launch_push_gather(const void* dc, ncclWindow_t win, size_t off_x, size_t off_dy,
-                                int slot, const void* X, const void* dY, int64_t cx, int64_t cy,
-                                tag_dtype_t in, tag_dtype_t wire, int max_ctas, cudaStream_t s) {
+tag_status_t launch_push_gather_group(const void* dc, const PushSegment* seg, int count, int slot,
+                                      tag_dtype_t in, tag_dtype_t wire, int max_ctas,
+                                      cudaStream_t s) {
+    if (count < 1 || count > MAX_GROUP) return fail(TAG_ERR_INVALID_ARG, "push group size");
     const ncclDevComm& comm = *static_cast<const ncclDevComm*>(dc);
     const int64_t ew = static_cast<int64_t>(dtype_size(wire));
-    const int64_t vx = cx * ew / 16, vy = cy * ew / 16;
-    const int grid = push_grid(vx + vy, max_ctas);
+    PushGroup g;
+    std::memset(&g, 0, sizeof g);
+    int64_t total = 0;
+    for (int i = 0; i < count; ++i) {
+        PushLayer& L = g.L[i];
+        L.X = seg[i].X;
+        L.dY = seg[i].dY;
+        L.win = static_cast<ncclWindow_t>(seg[i].win);
+        L.off_x = seg[i].off_x;
+        L.off_dy = seg[i].off_dy;
+        L.vx = seg[i].cx * ew / 16;
+        L.vy = seg[i].cy * ew / 16;
+        L.vbegin = total;
+        total += L.vx + L.vy;
+    }
+    g.count = count;
+    g.total = total;
+    g.slot = slot;
+    const int grid = push_grid(total, max_ctas);
     if (in == wire)
-        push_gather_kernel<false><<<grid, PUSH_THREADS, 0, s>>>(comm, win, off_x, off_dy, X, dY,
-                                                                 vx, vy, slot);
+        push_gather_kernel<false><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
     else
-        push_gather_kernel<true><<<grid, PUSH_THREADS, 0, s>>>(comm, win, off_x, off_dy, X, dY,
-                                                                vx, vy, slot);
+        push_gather_kernel<true><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "launch push_gather_kernel");
     count_launch();

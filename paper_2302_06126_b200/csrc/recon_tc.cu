@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 #include "ptx.cuh"
@@ -58,15 +59,40 @@ struct Cfg {
                                       (uint32_t(BM >> 4) << 24);
 };
 
-struct Params {
-    int M, N, K;
-    int num_n_blocks, num_tiles, num_k_blocks;
-    float alpha;
+// One launch reconstructs a group of layers (a gradient bucket): their output tiles are
+// concatenated in layer order and distributed round-robin over the persistent CTAs, so the
+// prologue, pipeline ramp-up and the last partial wave are paid once per bucket, not per layer.
+struct LayerParams {
+    CUtensorMap tmA;  // X_all (K x M) bf16, box 64 x BK, 128-B swizzle
+    CUtensorMap tmB;  // dY_all (K x N)
     void* C;          // dW out (may be nullptr with SGD)
     float* W;
     float* V;
+    int M, N;
+    int num_n_blocks, num_k_blocks;
+    int tile_begin;   // first global tile index of this layer
+    float alpha;
+};
+
+struct GroupParams {
+    LayerParams L[MAX_GROUP];
+    int count;
+    int num_tiles;
     float lr, mu, wd;
 };
+
+struct TileRef {
+    int li, m0, n0;
+};
+
+template <int BN>
+__device__ __forceinline__ TileRef locate(const GroupParams& gp, int tile) {
+    int li = 0;
+    while (li + 1 < gp.count && tile >= gp.L[li + 1].tile_begin) ++li;
+    const int t = tile - gp.L[li].tile_begin;
+    const int nnb = gp.L[li].num_n_blocks;
+    return TileRef{li, (t / nnb) * BM, (t % nnb) * BN};
+}
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);   // RNE, lo in the low half
@@ -82,8 +108,7 @@ __device__ __forceinline__ void grid_dep_launch() {
 
 template <int BN, bool OUT_BF16, bool SGD>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const Params p)
+recon_tc_kernel(const __grid_constant__ GroupParams gp)
 {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
@@ -106,8 +131,10 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
 
     // ---- prologue (overlaps the previous kernel's tail under programmatic dependent launch)
     if (warp == 0 && lane == 0) {
-        ptx::tma_prefetch_desc(&tmA);
-        ptx::tma_prefetch_desc(&tmB);
+        for (int i = 0; i < gp.count; ++i) {
+            ptx::tma_prefetch_desc(&gp.L[i].tmA);
+            ptx::tma_prefetch_desc(&gp.L[i].tmB);
+        }
         for (int s = 0; s < C::STAGES; ++s) {
             ptx::mbar_init(bar_full + 8 * s, 1);
             ptx::mbar_init(bar_empty + 8 * s, 1);
@@ -131,10 +158,12 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-                const int m0 = (tile / p.num_n_blocks) * BM;
-                const int n0 = (tile % p.num_n_blocks) * BN;
-                for (int kb = 0; kb < p.num_k_blocks; ++kb) {
+            for (int tile = blockIdx.x; tile < gp.num_tiles; tile += gridDim.x) {
+                const TileRef tr = locate<BN>(gp, tile);
+                const CUtensorMap* tmA = &gp.L[tr.li].tmA;
+                const CUtensorMap* tmB = &gp.L[tr.li].tmB;
+                const int nkb = gp.L[tr.li].num_k_blocks;
+                for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait(bar_empty + 8 * stage, phase ^ 1);
                     const uint32_t fb = bar_full + 8 * stage;
                     ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
@@ -142,10 +171,10 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                     const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
                     for (int c = 0; c < BM / 64; ++c)
-                        ptx::tma_load_2d(sa + c * CHUNK_BYTES, &tmA, fb, m0 + 64 * c, kb * BK);
+                        ptx::tma_load_2d(sa + c * CHUNK_BYTES, tmA, fb, tr.m0 + 64 * c, kb * BK);
 #pragma unroll
                     for (int c = 0; c < BN / 64; ++c)
-                        ptx::tma_load_2d(sb + c * CHUNK_BYTES, &tmB, fb, n0 + 64 * c, kb * BK);
+                        ptx::tma_load_2d(sb + c * CHUNK_BYTES, tmB, fb, tr.n0 + 64 * c, kb * BK);
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -157,11 +186,12 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            for (int tile = blockIdx.x; tile < gp.num_tiles; tile += gridDim.x) {
+                const int nkb = gp.L[locate<BN>(gp, tile).li].num_k_blocks;
                 ptx::mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);   // epilogue drained it
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int kb = 0; kb < p.num_k_blocks; ++kb) {
+                for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait(bar_full + 8 * stage, phase);        // TMA landed
                     ptx::tc_fence_after();
                     const uint32_t sa = s_stages + stage * C::STAGE_BYTES;
@@ -194,15 +224,16 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
         constexpr int COLS_PER_CHUNK = 128 / ESZ;               // 128 bytes of output per row
         constexpr int CHUNKS = (BN / 2) / COLS_PER_CHUNK;
         constexpr int VEC = 16 / ESZ;                           // output elements per 16 B
-        const float alpha = p.alpha;
         const int sub = lane >> 3;               // row within a 4-row group (write-out phase)
         const int cj = lane & 7;                 // 16-byte column slot (write-out phase)
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-            const int m0 = (tile / p.num_n_blocks) * BM;
-            const int n0 = (tile % p.num_n_blocks) * BN;
-            const int row0 = m0 + 32 * quad;     // first output row of this warp
+        for (int tile = blockIdx.x; tile < gp.num_tiles; tile += gridDim.x) {
+            const TileRef tr = locate<BN>(gp, tile);
+            const LayerParams& p = gp.L[tr.li];
+            const float alpha = p.alpha;
+            const int n0 = tr.n0;
+            const int row0 = tr.m0 + 32 * quad;  // first output row of this warp
             ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
             ptx::tc_fence_after();
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quad) << 16) + acc * BN;
@@ -272,9 +303,9 @@ recon_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
                         float* vf = reinterpret_cast<float*>(&vv);
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            const float g = __fadd_rn(dv[e], __fmul_rn(p.wd, wf[e]));
-                            vf[e] = __fadd_rn(__fmul_rn(p.mu, vf[e]), g);
-                            wf[e] = __fsub_rn(wf[e], __fmul_rn(p.lr, vf[e]));
+                            const float g = __fadd_rn(dv[e], __fmul_rn(gp.wd, wf[e]));
+                            vf[e] = __fadd_rn(__fmul_rn(gp.mu, vf[e]), g);
+                            wf[e] = __fsub_rn(wf[e], __fmul_rn(gp.lr, vf[e]));
                         }
                         __stcs(wp, wv);
                         __stcs(vp, vv);
@@ -324,27 +355,32 @@ bool encode_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esiz
 }
 
 template <int BN, bool OUT_BF16, bool SGD>
-tag_status_t launch_t(const ReconArgs& a, cudaStream_t s) {
+tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s) {
     using C = Cfg<BN>;
-    CUtensorMap tmA, tmB;
-    if (!encode_2d(&tmA, a.A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.K, a.M, 64, BK) ||
-        !encode_2d(&tmB, a.Bm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a.K, a.N, 64, BK))
-        return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
-    Params p;
-    p.M = static_cast<int>(a.M);
-    p.N = static_cast<int>(a.N);
-    p.K = static_cast<int>(a.K);
-    p.num_n_blocks = static_cast<int>((a.N + BN - 1) / BN);
-    const int num_m_blocks = static_cast<int>((a.M + BM - 1) / BM);
-    p.num_tiles = num_m_blocks * p.num_n_blocks;
-    p.num_k_blocks = static_cast<int>((a.K + BK - 1) / BK);
-    p.alpha = a.alpha;
-    p.C = a.C;
-    p.W = a.W;
-    p.V = a.V;
-    p.lr = a.lr;
-    p.mu = a.mu;
-    p.wd = a.wd;
+    GroupParams gp;
+    std::memset(&gp, 0, sizeof gp);
+    int tiles = 0;
+    for (int i = 0; i < count; ++i) {
+        LayerParams& L = gp.L[i];
+        if (!encode_2d(&L.tmA, a[i].A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a[i].K, a[i].M, 64, BK) ||
+            !encode_2d(&L.tmB, a[i].Bm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a[i].K, a[i].N, 64, BK))
+            return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
+        L.C = a[i].C;
+        L.W = a[i].W;
+        L.V = a[i].V;
+        L.M = static_cast<int>(a[i].M);
+        L.N = static_cast<int>(a[i].N);
+        L.num_n_blocks = static_cast<int>((a[i].N + BN - 1) / BN);
+        L.num_k_blocks = static_cast<int>((a[i].K + BK - 1) / BK);
+        L.tile_begin = tiles;
+        L.alpha = a[i].alpha;
+        tiles += static_cast<int>((a[i].M + BM - 1) / BM) * L.num_n_blocks;
+    }
+    gp.count = count;
+    gp.num_tiles = tiles;
+    gp.lr = a[0].lr;
+    gp.mu = a[0].mu;
+    gp.wd = a[0].wd;
     auto kern = recon_tc_kernel<BN, OUT_BF16, SGD>;
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
@@ -354,7 +390,7 @@ tag_status_t launch_t(const ReconArgs& a, cudaStream_t s) {
         attr_set = true;
     }
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(p.num_tiles < num_sms() ? p.num_tiles : num_sms()));
+    cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms() ? tiles : num_sms()));
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = s;
@@ -363,7 +399,7 @@ tag_status_t launch_t(const ReconArgs& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, tmA, tmB, p);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, gp);
     if (e != cudaSuccess) return cuda_fail(e, "launch recon_tc_kernel");
     count_launch();
     return TAG_OK;
@@ -384,15 +420,26 @@ bool recon_tc_ok(const ReconArgs& a) {
     return true;
 }
 
-tag_status_t launch_recon_tc(const ReconArgs& a, cudaStream_t s) {
+tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s) {
+    if (count < 1 || count > MAX_GROUP) return fail(TAG_ERR_INVALID_ARG, "recon group size");
+    int64_t kmax = 0;
+    for (int i = 0; i < count; ++i) {
+        if (a[i].sgd != a[0].sgd || a[i].out != a[0].out)
+            return fail(TAG_ERR_INVALID_ARG, "recon group: mixed epilogues");
+        kmax = a[i].K > kmax ? a[i].K : kmax;
+    }
     // Small K (the HBM-write-bound regime of the paper's small-batch layers): BN = 128 tiles,
     // 4 TMEM accumulators, finer tail. Large K (tensor-bound): BN = 256 halves the smem operand
     // traffic per MMA, 2 accumulators.
-    const bool wide = a.K > 256;
-    if (a.sgd) return wide ? launch_t<256, false, true>(a, s) : launch_t<128, false, true>(a, s);
-    if (a.out == TAG_BF16)
-        return wide ? launch_t<256, true, false>(a, s) : launch_t<128, true, false>(a, s);
-    return wide ? launch_t<256, false, false>(a, s) : launch_t<128, false, false>(a, s);
+    const bool wide = kmax > 256;
+    if (a[0].sgd) return wide ? launch_t<256, false, true>(a, count, s) : launch_t<128, false, true>(a, count, s);
+    if (a[0].out == TAG_BF16)
+        return wide ? launch_t<256, true, false>(a, count, s) : launch_t<128, true, false>(a, count, s);
+    return wide ? launch_t<256, false, false>(a, count, s) : launch_t<128, false, false>(a, count, s);
+}
+
+tag_status_t launch_recon_tc(const ReconArgs& a, cudaStream_t s) {
+    return launch_recon_tc_group(&a, 1, s);
 }
 
 }  // namespace tag

@@ -43,6 +43,9 @@ struct ReconArgs {
 // Tensor-core path (tcgen05 + TMEM + TMA). Requires 16-byte aligned rows (see recon_tc_ok).
 bool recon_tc_ok(const ReconArgs& a);
 tag_status_t launch_recon_tc(const ReconArgs& a, cudaStream_t s);
+// Grouped form: one persistent launch over all layers' tiles (1 <= count <= MAX_GROUP).
+constexpr int MAX_GROUP = 8;
+tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s);
 // SIMT FFMA path: any shape, fp32 or bf16 operands (exact fp32 accumulation in k order).
 tag_status_t launch_recon_simt(const ReconArgs& a, cudaStream_t s);
 
@@ -51,6 +54,18 @@ tag_status_t launch_recon_simt(const ReconArgs& a, cudaStream_t s);
 // dtypes match. Counts are elements.
 tag_status_t launch_pack(const void* x, void* x_dst, int64_t nx, const void* dy, void* dy_dst,
                          int64_t ny, tag_dtype_t in, tag_dtype_t wire, cudaStream_t s);
+
+// ------------------------------------------------------------------ NVLink push gather (a1+a2)
+struct PushSegment {
+    const void* X;
+    const void* dY;
+    void* win;              // ncclWindow_t
+    size_t off_x, off_dy;   // byte offsets of this buffer's X_all / dY_all in the window
+    int64_t cx, cy;         // elements of this rank's X_r / dY_r
+};
+tag_status_t launch_push_gather_group(const void* dc, const PushSegment* seg, int count, int slot,
+                                      tag_dtype_t in, tag_dtype_t wire, int max_ctas,
+                                      cudaStream_t s);
 
 // ------------------------------------------------------------------ unfused SGD
 tag_status_t launch_sgd(const float* dW, float* W, float* V, int64_t len, float lr, float mu,

@@ -77,6 +77,11 @@ _SIGS = {
     "tag_dense_allreduce": ([_vp, _vp, _vp], _st),
     "tag_sgd_step": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_select": ([_p(LayerDesc), _i, _p(Topology), _p(_i)], _st),
+    "tag_sfb_group_create": ([_p(_vp), _i, _p(_vp)], _st),
+    "tag_sfb_group_destroy": ([_vp], _st),
+    "tag_sfb_group_sync": ([_vp, _p(_vp), _p(_vp), _p(_vp), _vp], _st),
+    "tag_sfb_group_gather": ([_vp, _p(_vp), _p(_vp), _vp], _st),
+    "tag_sfb_group_reconstruct": ([_vp, _p(_vp), _vp], _st),
 }
 for _name, (_args, _res) in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -248,6 +253,47 @@ class SfbPlan:
     def close(self):
         if self._h:
             _check(_lib.tag_sfb_plan_destroy(self._h), "tag_sfb_plan_destroy")
+            self._h = None
+
+
+class SfbGroup:
+    """A bucket of plans synchronised by one push kernel and one reconstruction launch."""
+
+    def __init__(self, plans):
+        self.plans = list(plans)
+        arr = (_vp * len(self.plans))(*[p._h for p in self.plans])
+        h = _vp()
+        _check(_lib.tag_sfb_group_create(arr, len(self.plans), ctypes.byref(h)),
+               "tag_sfb_group_create")
+        self._h = h
+
+    def _ptrs(self, ts, which):
+        out = []
+        for p, t in zip(self.plans, ts):
+            if which == "X":
+                out.append(_dev(t, p.in_torch, (p.B, p.M), "X"))
+            elif which == "dY":
+                out.append(_dev(t, p.in_torch, (p.B, p.N), "dY"))
+            else:
+                out.append(_dev(t, p.out_torch, (p.M, p.N), "dW"))
+        assert len(out) == len(self.plans), f"{which}: one tensor per plan"
+        return (_vp * len(out))(*out)
+
+    def sync(self, Xs, dYs, dWs, stream=None):
+        _check(_lib.tag_sfb_group_sync(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"),
+                                       self._ptrs(dWs, "dW"), _stream(stream)), "tag_sfb_group_sync")
+
+    def gather(self, Xs, dYs, stream=None):
+        _check(_lib.tag_sfb_group_gather(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"),
+                                         _stream(stream)), "tag_sfb_group_gather")
+
+    def reconstruct(self, dWs, stream=None):
+        _check(_lib.tag_sfb_group_reconstruct(self._h, self._ptrs(dWs, "dW"), _stream(stream)),
+               "tag_sfb_group_reconstruct")
+
+    def close(self):
+        if self._h:
+            _check(_lib.tag_sfb_group_destroy(self._h), "tag_sfb_group_destroy")
             self._h = None
 
 

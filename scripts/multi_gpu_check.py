@@ -117,6 +117,29 @@ def main():
     record("fused_sgd", torch.equal(W1, W2) and torch.equal(v1, v2) and len(set(hashes)) == 1)
     plan.close()
 
+    # 8: a bucket (one push kernel + one reconstruction launch) == per-layer syncs, bit for bit
+    specs = [(25088, 4096, 32, "relu", "masked_small"), (4096, 4096, 32, "relu", "masked_small"),
+             (4096, 1000, 32, "relu", "softmax_onehot"), (520, 264, 24, "int3", "int3")]
+    plans, Xs, dYs, refs, outs = [], [], [], [], []
+    for li, (M, N, B, xd, dyd) in enumerate(specs):
+        X, dY = synth.factors(2, 10 + li, rank, M, N, B, xd, dyd)
+        plans.append(tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32"))
+        Xs.append(torch.from_numpy(X).to(torch.bfloat16).cuda())
+        dYs.append(torch.from_numpy(dY).to(torch.bfloat16).cuda())
+        refs.append(torch.empty(M, N, device="cuda"))
+        outs.append(torch.full((M, N), float("nan"), device="cuda"))
+        plans[-1].sync(Xs[-1], dYs[-1], refs[-1])
+    group = tag.SfbGroup(plans)
+    for _ in range(3):
+        group.sync(Xs, dYs, outs)
+    torch.cuda.synchronize()
+    same = all(torch.equal(r, o) for r, o in zip(refs, outs))
+    hashes = tdist.all_gather_object("".join(digest(o) for o in outs))
+    record("group_bucket", same and len(set(hashes)) == 1)
+    group.close()
+    for p in plans:
+        p.close()
+
     # 7: selector identical on all ranks and equal to the oracle
     lays = [dict(M=L.M, N=L.N, B=L.B) for c in (2, 3, 4, 5) for L in synth.CONFIGS[c].layers]
     got = tag.select([dict(l, factor_dtype="bf16", grad_dtype="f32") for l in lays], n,

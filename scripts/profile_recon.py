@@ -17,8 +17,30 @@ ap.add_argument("--n", type=int, default=1, help="virtual replicas (K = n*B)")
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--out", default="f32")
 ap.add_argument("--sgd", action="store_true")
+ap.add_argument("--group", action="store_true", help="all layers of the config in one bucket")
 a = ap.parse_args()
 cfg = synth.CONFIGS[a.config]
+if a.group:
+    comm = tag.Comm(1, 0, 0)
+    plans, Xs, dYs, dWs = [], [], [], []
+    for li, L in enumerate(cfg.layers):
+        X, dY = synth.all_factors(cfg.cid, li, a.n, L.M, L.N, L.B, L.x_dist, L.dy_dist)
+        K = a.n * L.B
+        plans.append(tag.SfbPlan(comm, L.M, L.N, K, "bf16", "bf16", a.out))
+        Xs.append(torch.from_numpy(X.reshape(K, L.M)).to(torch.bfloat16).cuda())
+        dYs.append(torch.from_numpy(dY.reshape(K, L.N)).to(torch.bfloat16).cuda())
+        dWs.append(torch.empty(L.M, L.N, dtype=torch.float32 if a.out == "f32" else torch.bfloat16,
+                               device="cuda"))
+    g = tag.SfbGroup(plans)
+    for _ in range(a.iters):
+        g.sync(Xs, dYs, dWs)
+    torch.cuda.synchronize()
+    print(f"ok group config {a.config} n={a.n} iters={a.iters}")
+    g.close()
+    for p in plans:
+        p.close()
+    comm.close()
+    sys.exit(0)
 li, L = next((i, L) for i, L in enumerate(cfg.layers) if L.name == a.layer)
 X, dY = synth.all_factors(cfg.cid, li, a.n, L.M, L.N, L.B, L.x_dist, L.dy_dist)
 comm = tag.Comm(1, 0, 0)

@@ -260,3 +260,50 @@ def test_launch_counter_counts_kernels(tag, comm1):
     assert tag.kernel_launches() - before == 1          # n = 1, bf16 in == wire: recon only
     assert torch.all(dW == 1.0)                          # X = dY = 1 -> dW = 1 (scale pin)
     plan.close()
+
+
+@pytest.mark.parametrize("layers,out_dt", [
+    ([(25088, 4096, 32), (4096, 4096, 32), (4096, 1000, 32)], "f32"),      # VGG-19 FC bucket
+    ([(512, 32000, 256), (512, 2048, 256), (2048, 512, 256)], "bf16"),     # Transformer bucket
+    ([(136, 264, 40), (130, 257, 10), (8, 8, 1)], "f32"),                  # mixed TC + SIMT shapes
+])
+def test_group_equals_per_plan(tag, comm1, layers, out_dt):
+    """One push + one persistent launch for a bucket == tag_sfb_sync per layer, bit for bit."""
+    plans, Xs, dYs, ref, got = [], [], [], [], []
+    for li, (M, N, K) in enumerate(layers):
+        X = synth.draw("normal", K, M, synth.rng(70, li, 0, 0))
+        dY = synth.draw("small", K, N, synth.rng(70, li, 0, 1))
+        plan = tag.SfbPlan(comm1, M, N, K, "bf16", "bf16", out_dt)
+        plans.append(plan)
+        Xs.append(to_dev(X, "bf16"))
+        dYs.append(to_dev(dY, "bf16"))
+        r = torch.empty(M, N, dtype=TORCH[out_dt], device="cuda")
+        plan.sync(Xs[-1], dYs[-1], r)
+        ref.append(r)
+        got.append(torch.full((M, N), float("nan"), dtype=TORCH[out_dt], device="cuda"))
+    group = tag.SfbGroup(plans)
+    before = tag.kernel_launches()
+    group.sync(Xs, dYs, got)
+    torch.cuda.synchronize()
+    launches = tag.kernel_launches() - before
+    if all(p.info()["tensor_cores"] for p in plans):
+        assert launches == 1                 # n = 1, no cast: one grouped reconstruction
+    for r, g in zip(ref, got):
+        assert torch.equal(r, g)
+    group.close()
+    for p in plans:
+        p.close()
+
+
+def test_group_validation(tag, comm1):
+    a = tag.SfbPlan(comm1, 64, 32, 8, "bf16", "bf16", "f32")
+    b = tag.SfbPlan(comm1, 64, 32, 8, "bf16", "bf16", "bf16")
+    with pytest.raises(tag.TagError) as e:
+        tag.SfbGroup([a, b])                       # mixed out dtypes
+    assert e.value.status == tag.ERR_INVALID_ARG
+    with pytest.raises(tag.TagError):
+        tag.SfbGroup([a, a])                       # duplicate plan
+    with pytest.raises(tag.TagError):
+        tag.SfbGroup([])
+    a.close()
+    b.close()
