@@ -148,6 +148,43 @@ def run_reference(args, cfg, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def virtual_n_recon(tag, comm, cfg, nv, stream, flush_l2, start_events, peaks, iters=20):
+    """Reconstruction-only timing at K = nv*B on one GPU (nv virtual replicas' factors stacked
+    rank-major), fp32 and bf16 dW, each layer alone; fractions of the tensor and HBM roofs."""
+    out = {}
+    for out_dt in ("f32", "bf16"):
+        res = {}
+        for li, L in enumerate(cfg.layers):
+            K = nv * L.B
+            X, dY = synth.all_factors(cfg.cid, li, nv, L.M, L.N, L.B, L.x_dist, L.dy_dist)
+            plan = tag.SfbPlan(comm, L.M, L.N, K, "bf16", "bf16", out_dt)
+            Xd = torch.from_numpy(X.reshape(K, L.M)).to(torch.bfloat16).cuda()
+            dYd = torch.from_numpy(dY.reshape(K, L.N)).to(torch.bfloat16).cuda()
+            dW = torch.empty(L.M, L.N, dtype=torch.float32 if out_dt == "f32" else torch.bfloat16,
+                             device="cuda")
+            plan.gather(Xd, dYd, stream)
+            for _ in range(3):
+                plan.reconstruct(dW, stream)
+            ts = []
+            for _ in range(iters):
+                evs = start_events(2)
+                plan.reconstruct(dW, stream)
+                evs[1].record(stream)
+                torch.cuda.synchronize()
+                ts.append(evs[0].elapsed_time(evs[1]))
+            t = statistics.median(ts) * 1e-3
+            flops = 2.0 * L.M * L.N * K
+            byts = K * (L.M + L.N) * 2 + L.M * L.N * ESIZE[out_dt]
+            res[L.name] = {"K": K, "us": round(t * 1e6, 2),
+                           "tensor_frac": round(flops / t / 1e12 / peaks["bf16_tflops"], 4),
+                           "hbm_frac": round(byts / t / 1e9 / peaks["hbm_gbs"], 4),
+                           "ideal_tensor_us": round(flops / (peaks["bf16_tflops"] * 1e12) * 1e6, 2),
+                           "ideal_hbm_us": round(byts / (peaks["hbm_gbs"] * 1e9) * 1e6, 2)}
+            plan.close()
+        out[f"dW_{out_dt}"] = res
+    return out
+
+
 def config_json(cfg, n, args):
     return {"workload": f"{cfg.name} sync (configs[{cfg.cid - 1}]), n={n}",
             "layers": [f"{L.name} {L.M}x{L.N}" for L in cfg.layers], "rows_per_gpu": cfg.layers[0].B,
@@ -166,6 +203,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--ref-mac", type=float, default=2.5e10)
+    ap.add_argument("--no-virtual", action="store_true")
     ap.add_argument("--per-layer-step", action="store_true",
                     help="time the step as one tag_sfb_sync per layer instead of one bucket")
     args = ap.parse_args()
@@ -379,6 +417,13 @@ def main():
            "ms_per_step": round(t_e2e, 4), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "api": "tag_sfb_sync_host (pinned host X, dY in; full dW out)"}
 
+    # ---------------------------------------------------------------- virtual n = 8 (1 GPU)
+    # north_star's target point is fc6 at n = 8 (K = 256); with one GPU the reconstruction of that
+    # point is timed on K = 8*32 stacked factor rows (identical contraction and alpha = 1/(8B))
+    virt = None
+    if n == 1 and not args.no_virtual:
+        virt = virtual_n_recon(tag, comm, cfg, 8, stream, flush_l2, start_events, peaks)
+
     clocks = clk.summary()
     cpu = None
     if rank == 0 and n == 1 and not args.no_cpu_baseline:
@@ -391,6 +436,7 @@ def main():
                 "dtype": cfg.wire_dtype, "data": "synthetic", "config": config_json(cfg, n, args),
                 "per_layer": per_layer, "roofline": roofline, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
+                "virtual_n8_recon": virt,
                 "lib": tag.version()}
         print(json.dumps(line), flush=True)
     if group is not None:

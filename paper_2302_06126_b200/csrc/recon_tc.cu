@@ -40,7 +40,7 @@ constexpr int BK = 32;                   // factor rows per pipeline stage
 constexpr int NUM_EPI_WARPS = 8;
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;   // 320
 constexpr int CHUNK_BYTES = BK * 128;    // one 128-byte-wide MN chunk of BK rows (4 KB)
-constexpr int EPI_BUF_BYTES = 32 * 128;  // 32 rows x 128 B transpose buffer per epilogue warp
+constexpr int EPI_BUF_BYTES = 2 * 32 * 128;  // 2 x (32 rows x 128 B) transpose buffers per warp
 constexpr int TMEM_COLS = 512;
 
 template <int BN>
@@ -224,21 +224,28 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp)
         constexpr int COLS_PER_CHUNK = 128 / ESZ;               // 128 bytes of output per row
         constexpr int CHUNKS = (BN / 2) / COLS_PER_CHUNK;
         constexpr int VEC = 16 / ESZ;                           // output elements per 16 B
+        constexpr int PAIR = OUT_BF16 ? 1 : 2;                  // chunks staged per round
         const int sub = lane >> 3;               // row within a 4-row group (write-out phase)
         const int cj = lane & 7;                 // 16-byte column slot (write-out phase)
         int acc = 0;
         uint32_t acc_phase = 0;
+        const float lr = gp.lr, mu = gp.mu, wd = gp.wd;
         for (int tile = blockIdx.x; tile < gp.num_tiles; tile += gridDim.x) {
             const TileRef tr = locate<BN>(gp, tile);
-            const LayerParams& p = gp.L[tr.li];
-            const float alpha = p.alpha;
+            // this tile's layer parameters, read once into registers
+            const LayerParams& lp = gp.L[tr.li];
+            uint8_t* const Cp = static_cast<uint8_t*>(lp.C);
+            float* const Wp = lp.W;
+            float* const Vp = lp.V;
+            const int M = lp.M, N = lp.N;
+            const float alpha = lp.alpha;
             const int n0 = tr.n0;
             const int row0 = tr.m0 + 32 * quad;  // first output row of this warp
             ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
             ptx::tc_fence_after();
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quad) << 16) + acc * BN;
             // chunks of this warp's column half that hold any output column (warp-uniform)
-            int nch = (p.N - (n0 + half * (BN / 2)) + COLS_PER_CHUNK - 1) / COLS_PER_CHUNK;
+            int nch = (N - (n0 + half * (BN / 2)) + COLS_PER_CHUNK - 1) / COLS_PER_CHUNK;
             nch = nch < 0 ? 0 : (nch > CHUNKS ? CHUNKS : nch);
             if (nch == 0) {                       // nothing to read: release the accumulator
                 ptx::tc_fence_before();
@@ -246,73 +253,93 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp)
                 if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
             }
 #pragma unroll 1
-            for (int ch = 0; ch < nch; ++ch) {
-                const int col = half * (BN / 2) + ch * COLS_PER_CHUNK;   // within the tile
-                uint32_t w[32];                                          // 128 B of this row
-                if constexpr (OUT_BF16) {
-                    uint32_t r0[32], r1[32];
-                    ptx::tmem_ld_32x32b_x32(t_row + col, r0);
-                    ptx::tmem_ld_32x32b_x32(t_row + col + 32, r1);
-                    ptx::tmem_wait_ld();
+            for (int ch = 0; ch < nch; ch += PAIR) {
+                const int np = (nch - ch) < PAIR ? (nch - ch) : PAIR;    // chunks this round
+                uint32_t w[PAIR][32];                                    // 128 B of row per chunk
+                // ---- TMEM -> registers: every load of the round issued before one wait
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        w[i] = pack_bf16x2(__fmul_rn(__uint_as_float(r0[2 * i]), alpha),
-                                           __fmul_rn(__uint_as_float(r0[2 * i + 1]), alpha));
-                        w[16 + i] = pack_bf16x2(__fmul_rn(__uint_as_float(r1[2 * i]), alpha),
-                                                __fmul_rn(__uint_as_float(r1[2 * i + 1]), alpha));
+                for (int q = 0; q < PAIR; ++q) {
+                    if (q >= np) break;
+                    const uint32_t tc = t_row + half * (BN / 2) + (ch + q) * COLS_PER_CHUNK;
+                    if constexpr (OUT_BF16) {
+                        uint32_t r0[32], r1[32];
+                        ptx::tmem_ld_32x32b_x32(tc, r0);
+                        ptx::tmem_ld_32x32b_x32(tc + 32, r1);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            w[q][i] = pack_bf16x2(__fmul_rn(__uint_as_float(r0[2 * i]), alpha),
+                                                  __fmul_rn(__uint_as_float(r0[2 * i + 1]), alpha));
+                            w[q][16 + i] = pack_bf16x2(__fmul_rn(__uint_as_float(r1[2 * i]), alpha),
+                                                       __fmul_rn(__uint_as_float(r1[2 * i + 1]), alpha));
+                        }
+                    } else {
+                        ptx::tmem_ld_32x32b_x32(tc, w[q]);
                     }
-                } else {
-                    ptx::tmem_ld_32x32b_x32(t_row + col, w);
+                }
+                if constexpr (!OUT_BF16) {
                     ptx::tmem_wait_ld();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        w[i] = __float_as_uint(__fmul_rn(__uint_as_float(w[i]), alpha));
+                    for (int q = 0; q < PAIR; ++q)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            w[q][i] = __float_as_uint(__fmul_rn(__uint_as_float(w[q][i]), alpha));
                 }
-                if (ch == nch - 1) {
+                if (ch + np >= nch) {
                     // last TMEM read of this accumulator by this warp: hand it back to the MMA
                     ptx::tc_fence_before();
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
                 }
-                __syncwarp();                     // previous chunk's smem reads are done
-                const uint32_t rowaddr = sbuf + lane * 128;
+                // ---- registers -> 128B-swizzled smem (row `lane`), conflict-free
+                __syncwarp();                     // previous round's smem reads are done
 #pragma unroll
-                for (int j = 0; j < 8; ++j)       // 16-byte slot j of row `lane`, swizzled
-                    ptx::st_shared_v4(rowaddr + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1],
-                                      w[4 * j + 2], w[4 * j + 3]);
+                for (int q = 0; q < PAIR; ++q) {
+                    if (q >= np) break;
+                    const uint32_t rowaddr = sbuf + q * 4096 + lane * 128;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        ptx::st_shared_v4(rowaddr + ((j ^ (lane & 7)) << 4), w[q][4 * j],
+                                          w[q][4 * j + 1], w[q][4 * j + 2], w[q][4 * j + 3]);
+                }
                 __syncwarp();
-                const int gcol = n0 + col + cj * VEC;
-                const bool col_ok = gcol < p.N;   // N % 8 == 0: a 16-byte slot is all in or out
+                // ---- smem -> global: lane reads 16 B of row 4i+sub; 4 full lines per store
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int r = 4 * i + sub;
-                    const int grow = row0 + r;
-                    uint32_t a, b, c, d;
-                    ptx::ld_shared_v4(sbuf + r * 128 + ((cj ^ (r & 7)) << 4), a, b, c, d);
-                    if (!col_ok || grow >= p.M) continue;
-                    const int64_t off = static_cast<int64_t>(grow) * p.N + gcol;
-                    if constexpr (SGD) {
-                        // E2 (R14): g = dW + wd*W ; v = mu*v + g ; W -= lr*v   (fp32)
-                        float4* wp = reinterpret_cast<float4*>(p.W + off);
-                        float4* vp = reinterpret_cast<float4*>(p.V + off);
-                        float4 wv = __ldcs(wp);
-                        float4 vv = __ldcs(vp);
-                        const float dv[4] = {__uint_as_float(a), __uint_as_float(b),
-                                             __uint_as_float(c), __uint_as_float(d)};
-                        float* wf = reinterpret_cast<float*>(&wv);
-                        float* vf = reinterpret_cast<float*>(&vv);
+                for (int q = 0; q < PAIR; ++q) {
+                    if (q >= np) break;
+                    const int gcol = n0 + half * (BN / 2) + (ch + q) * COLS_PER_CHUNK + cj * VEC;
+                    const bool col_ok = gcol < N;   // N % 8 == 0: a 16-B slot is all in or out
+                    const int64_t off0 = static_cast<int64_t>(row0 + sub) * N + gcol;
+                    const int64_t step = 4 * static_cast<int64_t>(N);
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float g = __fadd_rn(dv[e], __fmul_rn(gp.wd, wf[e]));
-                            vf[e] = __fadd_rn(__fmul_rn(gp.mu, vf[e]), g);
-                            wf[e] = __fsub_rn(wf[e], __fmul_rn(gp.lr, vf[e]));
+                    for (int i = 0; i < 8; ++i) {
+                        const int r = 4 * i + sub;
+                        uint32_t a, b, c, d;
+                        ptx::ld_shared_v4(sbuf + q * 4096 + r * 128 + ((cj ^ (r & 7)) << 4), a, b, c, d);
+                        if (!col_ok || row0 + r >= M) continue;
+                        const int64_t off = off0 + i * step;
+                        if constexpr (SGD) {
+                            // E2 (R14): g = dW + wd*W ; v = mu*v + g ; W -= lr*v   (fp32)
+                            float4* wp = reinterpret_cast<float4*>(Wp + off);
+                            float4* vp = reinterpret_cast<float4*>(Vp + off);
+                            float4 wv = __ldcs(wp);
+                            float4 vv = __ldcs(vp);
+                            const float dv[4] = {__uint_as_float(a), __uint_as_float(b),
+                                                 __uint_as_float(c), __uint_as_float(d)};
+                            float* wf = reinterpret_cast<float*>(&wv);
+                            float* vf = reinterpret_cast<float*>(&vv);
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float g = __fadd_rn(dv[e], __fmul_rn(wd, wf[e]));
+                                vf[e] = __fadd_rn(__fmul_rn(mu, vf[e]), g);
+                                wf[e] = __fsub_rn(wf[e], __fmul_rn(lr, vf[e]));
+                            }
+                            __stcs(wp, wv);
+                            __stcs(vp, vv);
+                            if (Cp == nullptr) continue;
                         }
-                        __stcs(wp, wv);
-                        __stcs(vp, vv);
-                        if (p.C == nullptr) continue;
+                        __stcs(reinterpret_cast<uint4*>(Cp + off * ESZ), make_uint4(a, b, c, d));
                     }
-                    __stcs(reinterpret_cast<uint4*>(static_cast<uint8_t*>(p.C) + off * ESZ),
-                           make_uint4(a, b, c, d));
                 }
             }
             if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
