@@ -33,6 +33,7 @@ import torch  # noqa: E402
 
 from paper_2302_06126_b200 import dist as tdist  # noqa: E402
 from paper_2302_06126_b200 import synth  # noqa: E402
+import torch.distributed as dist  # noqa: E402
 
 METRIC = "per-layer SFB grad-sync us & dW GB/s (VGG-19 fc6/fc7/fc8, B=32/GPU)"
 ESIZE = {"f32": 4, "bf16": 2}
@@ -243,6 +244,7 @@ def main():
         flush_rd.sum()
     nl = len(layers)
 
+    sync_tok = torch.zeros(1, device="cuda")
     Xs, dYs, dWs = [l["X"] for l in layers], [l["dY"] for l in layers], [l["dW"] for l in layers]
     # the step is one bucket: one push kernel (n > 1) + one persistent reconstruction launch
     group = None if args.per_layer_step else tag.SfbGroup([l["plan"] for l in layers])
@@ -267,6 +269,10 @@ def main():
             # a ~40 us device spin ahead of the start event lets the host enqueue the whole step,
             # so the interval measures device time, not Python launch latency
             torch.cuda._sleep(SPIN_CYCLES)
+            if n > 1:
+                # device-side barrier (1-element NCCL all-reduce, ordered before the start event)
+                # so the inter-process launch skew is not timed as gather latency
+                dist.all_reduce(sync_tok)
         evs[0].record(stream)
         return evs
 
@@ -374,13 +380,7 @@ def main():
             L = l["L"]
             t = []
             for _ in range(max(3, min(args.steps, 10))):
-                flush_l2()
-                torch.cuda.synchronize()
-                tdist.barrier()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                with torch.cuda.stream(stream):
-                    torch.cuda._sleep(SPIN_CYCLES)
-                e0.record(stream)
+                e0, e1 = start_events(2)
                 l["plan"].local_grad(l["X"], l["dY"], l["dW"], stream)
                 l["plan"].dense_allreduce(l["dW"], stream)
                 e1.record(stream)

@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -214,8 +215,10 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp)
         }
     } else {
         // ===================================================== epilogue warps
-        // TMEM -> registers (one output row per lane) -> scale -> 128B-swizzled smem transpose
-        // -> coalesced 16-byte streaming stores, four full 128-byte lines per warp instruction.
+        // TMEM -> registers (one output row per lane) -> x alpha (-> RNE bf16) -> 128B-swizzled
+        // smem transpose -> coalesced 16-byte streaming stores, four FULL 128-byte lines per warp
+        // instruction. (Measured: direct 8-byte stores from the 16x256b TMEM layout — whole
+        // 32-B sectors but 8 lines per instruction — write HBM ~15 % slower at K = 32.)
         const int ew = warp - 2;                 // 0..7
         const int quad = warp & 3;               // TMEM lane quadrant this warp may access
         const int half = ew >> 2;                // which half of the tile's columns
@@ -456,9 +459,11 @@ tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s
         kmax = a[i].K > kmax ? a[i].K : kmax;
     }
     // Small K (the HBM-write-bound regime of the paper's small-batch layers): BN = 128 tiles,
-    // 4 TMEM accumulators, finer tail. Large K (tensor-bound): BN = 256 halves the smem operand
-    // traffic per MMA, 2 accumulators.
-    const bool wide = kmax > 256;
+    // 4 TMEM accumulators, finer tail. K >= 192: BN = 256 cuts the A-operand re-reads from L2
+    // (L2 bandwidth binds first there: measured 102 -> 88 us for fc6 at K = 256) and the smem
+    // read rate per MMA (96 instead of 128 B/cycle); 2 accumulators.
+    bool wide = kmax >= 192;
+    if (const char* e = std::getenv("TAG_RECON_BN")) wide = std::atoi(e) == 256;   // experiments
     if (a[0].sgd) return wide ? launch_t<256, false, true>(a, count, s) : launch_t<128, false, true>(a, count, s);
     if (a[0].out == TAG_BF16)
         return wide ? launch_t<256, true, false>(a, count, s) : launch_t<128, true, false>(a, count, s);
