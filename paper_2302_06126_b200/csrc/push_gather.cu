@@ -20,6 +20,8 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "tag_internal.h"
@@ -52,16 +54,25 @@ struct PushGroup {
     int slot;               // this rank's slot (world rank)
 };
 
-template <bool CAST>
+// DBG (profiling only, TAG_PUSH_DEBUG): 1 = skip the data stores, 2 = skip the barrier,
+// 3 = full kernel + printf of %globaltimer phase stamps from a few CTAs.
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <bool CAST, int DBG = 0>
 __global__ void __launch_bounds__(PUSH_THREADS)
 push_gather_kernel(const ncclDevComm comm, const __grid_constant__ PushGroup g)
 {
+    const uint64_t t_start = DBG == 3 ? gtimer() : 0;
     const int npeers = comm.lsaSize;
     const int me = comm.lsaRank;
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
     int li = 0;
-    for (int64_t v = tid; v < g.total; v += nthreads) {
+    for (int64_t v = tid; v < (DBG == 1 ? 0 : g.total); v += nthreads) {
         while (li + 1 < g.count && v >= g.L[li + 1].vbegin) ++li;   // v only grows
         const PushLayer& L = g.L[li];
         const int64_t lv = v - L.vbegin;
@@ -85,8 +96,21 @@ push_gather_kernel(const ncclDevComm comm, const __grid_constant__ PushGroup g)
         }
     }
     // all of this CTA's stores are released to every peer; CTA b waits for CTA b everywhere
-    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x);
-    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    uint64_t t_data = 0;
+    if constexpr (DBG == 3) {
+        __syncthreads();
+        t_data = gtimer();
+    }
+    if constexpr (DBG != 2) {
+        ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x);
+        bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    }
+    if constexpr (DBG == 3) {
+        if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1 || blockIdx.x == gridDim.x / 2))
+            printf("push rank %d cta %d start %llu data +%llu barrier +%llu\n", me, blockIdx.x,
+                   (unsigned long long)t_start, (unsigned long long)(t_data - t_start),
+                   (unsigned long long)(gtimer() - t_data));
+    }
 }
 
 }  // namespace
@@ -148,7 +172,17 @@ tag_status_t launch_push_gather_group(const void* dc, const PushSegment* seg, in
     g.total = total;
     g.slot = slot;
     const int grid = push_grid(total, max_ctas);
-    if (in == wire)
+    static const int dbg = [] {
+        const char* e = std::getenv("TAG_PUSH_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (dbg == 1)
+        push_gather_kernel<false, 1><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
+    else if (dbg == 2)
+        push_gather_kernel<false, 2><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
+    else if (dbg == 3)
+        push_gather_kernel<false, 3><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
+    else if (in == wire)
         push_gather_kernel<false><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
     else
         push_gather_kernel<true><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
