@@ -251,13 +251,12 @@ def main():
     # the step is one bucket: one push kernel (n > 1) + one persistent reconstruction launch
     group = None if args.per_layer_step else tag.SfbGroup([l["plan"] for l in layers])
 
-    def step(ev_mid=None):
+    def step():
         with torch.cuda.stream(stream):
             if group is not None:
-                group.gather(Xs, dYs, stream)
-                if ev_mid is not None:
-                    ev_mid.record(stream)
-                group.reconstruct(dWs, stream)
+                # one call: at n > 1 a single fused kernel pushes the factors over NVLink and
+                # reconstructs every layer (tag_sfb_group_sync); at n = 1 the reconstruction only
+                group.sync(Xs, dYs, dWs, stream)
             else:
                 for l in layers:
                     l["plan"].sync(l["X"], l["dY"], l["dW"], stream)
@@ -279,17 +278,30 @@ def main():
         return evs
 
     def timed_steps(nsteps):
-        """Whole steps: [start, after gather (group mode), end] per step."""
-        step_ms, recon_ms = [], []
+        """Whole steps, [start, end] per step."""
+        step_ms = []
+        for _ in range(nsteps):
+            evs = start_events(2)
+            step()
+            evs[1].record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(evs[0].elapsed_time(evs[1]))
+        return step_ms
+
+    def timed_staged(nsteps):
+        """The bucket split in two calls: gather (push kernel + LSA barrier) | reconstruct."""
+        g_ms, r_ms = [], []
         for _ in range(nsteps):
             evs = start_events(3)
-            step(evs[1] if group is not None else None)
-            evs[2].record(stream)
+            with torch.cuda.stream(stream):
+                group.gather(Xs, dYs, stream)
+                evs[1].record(stream)
+                group.reconstruct(dWs, stream)
+                evs[2].record(stream)
             torch.cuda.synchronize()
-            step_ms.append(evs[0].elapsed_time(evs[2]))
-            if group is not None:
-                recon_ms.append(evs[1].elapsed_time(evs[2]))
-        return step_ms, recon_ms
+            g_ms.append(evs[0].elapsed_time(evs[1]))
+            r_ms.append(evs[1].elapsed_time(evs[2]))
+        return g_ms, r_ms
 
     def timed_layers(nsteps):
         """Per-layer staged pass: gather | reconstruct of each layer on its own."""
@@ -315,26 +327,31 @@ def main():
     tdist.barrier()
     launches0 = tag.kernel_launches()
     with ClockSampler(local_rank) as clk:
-        steps_ms, recon_ms = timed_steps(args.steps)
+        steps_ms = timed_steps(args.steps)
     launches = tag.kernel_launches() - launches0
     torch.cuda.synchronize()
     tdist.barrier()
-    layer_recon_ms, layer_sync_ms = timed_layers(max(5, min(args.steps, 30)))
+    nstaged = max(5, min(args.steps, 30))
+    layer_recon_ms, layer_sync_ms = timed_layers(nstaged)
+    staged_g_ms, staged_r_ms = timed_staged(nstaged) if group is not None else ([], [])
 
     t_step_ms = tdist.max_over_ranks(statistics.mean(steps_ms))
     dw_bytes = sum(l["L"].M * l["L"].N * ESIZE[cfg.out_dtype] for l in layers)
     value = n * dw_bytes / (t_step_ms * 1e-3) / 1e9
 
-    # roofline of the dominant kernel: the (grouped) reconstruction, HBM-bound at these shapes
+    # roofline of the dominant kernel. Bucket mode: the step is ONE launch of recon_tc_kernel
+    # (with the NVLink push fused in at n > 1), so its duration is the step's.
     alg_bytes = sum(n * l["L"].B * (l["L"].M + l["L"].N) * ESIZE[cfg.wire_dtype]
                     + l["L"].M * l["L"].N * ESIZE[cfg.out_dtype] for l in layers)
     if group is not None:
-        recon_total_ms = tdist.max_over_ranks(statistics.mean(recon_ms))
+        kernel_ms = t_step_ms
         launches_per_step = 1
+        recon_only_ms = tdist.max_over_ranks(statistics.mean(staged_r_ms))
     else:
-        recon_total_ms = tdist.max_over_ranks(sum(statistics.mean(r) for r in layer_recon_ms))
+        kernel_ms = tdist.max_over_ranks(sum(statistics.mean(r) for r in layer_recon_ms))
         launches_per_step = nl
-    achieved = alg_bytes / (recon_total_ms * 1e-3) / 1e9
+        recon_only_ms = kernel_ms
+    achieved = alg_bytes / (kernel_ms * 1e-3) / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "recon_traffic.json")
     if os.path.exists(tp):
@@ -342,13 +359,17 @@ def main():
             traffic = json.load(open(tp)).get(f"config{args.config}_n{n}")
         except Exception:
             traffic = None
-    roofline = {"kernel": "recon_tc_kernel (grouped tcgen05 reconstruction, fused 1/(nB) epilogue)",
+    roofline = {"kernel": ("recon_tc_kernel<FUSED> (NVLink push + tcgen05 reconstruction, one launch "
+                           "per bucket)" if (group is not None and n > 1) else
+                           "recon_tc_kernel (grouped tcgen05 reconstruction, fused 1/(nB) epilogue)"),
                 "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
                 "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_step": alg_bytes, "launches_per_step": launches_per_step,
-                "kernel_us": round(recon_total_ms * 1e3, 2),
-                "share_of_step": round(recon_total_ms / t_step_ms, 3)}
+                "kernel_us": round(kernel_ms * 1e3, 2),
+                "share_of_step": round(kernel_ms / t_step_ms, 3),
+                "recon_only_us": round(recon_only_ms * 1e3, 2),
+                "recon_only_hbm_frac": round(alg_bytes / (recon_only_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4)}
 
     per_layer = {}
     for i, l in enumerate(layers):
@@ -368,10 +389,9 @@ def main():
             "selector": {0: "allreduce", 1: "sfb", 2: "none"}[choices[i]],
             "gather": l["plan"].info()["gather"]}
     if group is not None and n > 1:
-        t_gather = tdist.max_over_ranks(statistics.mean(
-            [s_ - r_ for s_, r_ in zip(steps_ms, recon_ms)]))
+        t_gather = tdist.max_over_ranks(statistics.mean(staged_g_ms))
         ag_all = sum((n - 1) * l["L"].B * (l["L"].M + l["L"].N) * ESIZE[cfg.wire_dtype] for l in layers)
-        per_layer["bucket_gather"] = {"us": round(t_gather * 1e3, 2),
+        per_layer["bucket_gather_staged"] = {"us": round(t_gather * 1e3, 2),
                                       "ingress_MB": round(ag_all / 1e6, 3),
                                       "busbw_GBps": round(ag_all / (t_gather * 1e-3) / 1e9, 1),
                                       "frac_of_900": round(ag_all / (t_gather * 1e-3) / 900e9, 4)}

@@ -94,6 +94,8 @@ struct tag_plan_s {
     void* win_base = nullptr;
     ncclWindow_t win = nullptr;
     size_t win_buf_bytes = 0;      // one buffer = K*(M+N)*e_w
+    size_t win_flag_off = 0;       // two u32 arrival counters (one per buffer parity)
+    uint32_t flag_total[2] = {0, 0};   // counter value after every fused call so far, per parity
     int parity = 0;
     void* lx = nullptr;            // local cast scratch for tag_local_grad (B x M, B x N wire)
     void* ldy = nullptr;
@@ -247,6 +249,75 @@ tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int
     return launch_recon_simt(a, s);
 }
 
+// Fused path (a1 + a2 + a3 + a4 in ONE kernel): every plan gathers by NVLink push without a cast
+// and reconstructs on the tensor cores. The reconstruction kernel pushes this rank's factors
+// into every peer's window and waits, per layer, on arrival counters before loading its tiles.
+bool fusable(const tag_plan_s* p, void* dW) {
+    if (p->gather_mode != TAG_GATHER_NVLINK_PUSH || p->d.in_dtype != p->d.wire_dtype || !p->use_tc)
+        return false;
+    if (std::getenv("TAG_NO_FUSE")) return false;
+    ReconArgs a{};
+    a.A = p->win_base;
+    a.Bm = p->win_base;
+    a.C = dW;
+    a.M = p->d.M;
+    a.N = p->d.N;
+    a.K = p->K;
+    a.wire = p->d.wire_dtype;
+    a.out = p->d.out_dtype;
+    return recon_tc_ok(a);
+}
+
+tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* X,
+                        const void* const* dY, void* const* dW, bool sgd, float* W, float* V,
+                        cudaStream_t s) {
+    tag_comm_s* c = plans[0]->comm;
+    ReconArgs a[MAX_GROUP];
+    for (int i = 0; i < count; ++i) {
+        tag_plan_s* p = plans[i];
+        const size_t ew = dtype_size(p->d.wire_dtype);
+        const size_t off_x = static_cast<size_t>(p->parity) * p->win_buf_bytes;
+        const size_t off_dy = off_x + static_cast<size_t>(p->K * p->d.M) * ew;
+        a[i] = ReconArgs{};
+        a[i].A = static_cast<char*>(p->win_base) + off_x;
+        a[i].Bm = static_cast<char*>(p->win_base) + off_dy;
+        a[i].C = dW[i];
+        a[i].M = p->d.M;
+        a[i].N = p->d.N;
+        a[i].K = p->K;
+        a[i].wire = p->d.wire_dtype;
+        a[i].out = p->d.out_dtype;
+        a[i].alpha = p->alpha;
+        a[i].sgd = sgd;
+        a[i].W = W;
+        a[i].V = V;
+        a[i].lr = p->d.lr;
+        a[i].mu = p->d.momentum;
+        a[i].wd = p->d.weight_decay;
+        a[i].srcX = X[i];
+        a[i].srcY = dY[i];
+        a[i].win = p->win;
+        a[i].off_x = off_x;
+        a[i].off_dy = off_dy;
+        a[i].off_flag = p->win_flag_off + 4 * static_cast<size_t>(p->parity);
+        a[i].cx = p->d.B * p->d.M;
+        a[i].cy = p->d.B * p->d.N;
+    }
+    // every CTA of every rank adds 1 per layer: the counter grows by n * grid per call
+    const uint32_t inc = static_cast<uint32_t>(c->nranks) * static_cast<uint32_t>(recon_tc_grid(a, count));
+    for (int i = 0; i < count; ++i) a[i].flag_target = plans[i]->flag_total[plans[i]->parity] + inc;
+    FusedGather fg{c->nranks, c->rank};
+    TAG_TRY(launch_recon_tc_group(a, count, s, &fg));
+    for (int i = 0; i < count; ++i) {
+        tag_plan_s* p = plans[i];
+        p->flag_total[p->parity] += inc;
+        p->src_x = a[i].A;
+        p->src_dy = a[i].Bm;
+        p->parity ^= 1;
+    }
+    return TAG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -367,7 +438,8 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
     }
     if (p->gather_mode == TAG_GATHER_NVLINK_PUSH) {
         p->win_buf_bytes = static_cast<size_t>(p->K * (d->M + d->N)) * ew;
-        size_t bytes = 2 * p->win_buf_bytes;
+        p->win_flag_off = (2 * p->win_buf_bytes + 255) & ~static_cast<size_t>(255);
+        size_t bytes = p->win_flag_off + 256;
         bytes = (bytes + 4095) & ~static_cast<size_t>(4095);      // NCCL_WIN_REQUIRED_ALIGNMENT
         ncclResult_t r = ncclMemAlloc(&p->win_base, bytes);
         if (r == ncclSuccess)
@@ -467,6 +539,7 @@ tag_status_t tag_sfb_sync(tag_sfb_plan_t p, const void* X, const void* dY, void*
     TAG_TRY(set_device(p->comm));
     TAG_TRY(check_async(p->comm));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (fusable(p, dW_out)) return fused_sync(&p, 1, &X, &dY, &dW_out, false, nullptr, nullptr, s);
     TAG_TRY(do_gather(p, X, dY, s));
     return do_recon(p, dW_out, false, nullptr, nullptr, p->K, p->alpha, s);
 }
@@ -480,6 +553,7 @@ tag_status_t tag_sfb_sync_sgd(tag_sfb_plan_t p, const void* X, const void* dY, f
     TAG_TRY(set_device(p->comm));
     TAG_TRY(check_async(p->comm));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (fusable(p, dW_out)) return fused_sync(&p, 1, &X, &dY, &dW_out, true, W, v, s);
     TAG_TRY(do_gather(p, X, dY, s));
     return do_recon(p, dW_out, true, W, v, p->K, p->alpha, s);
 }
@@ -688,7 +762,18 @@ tag_status_t tag_sfb_group_reconstruct(tag_sfb_group_t g, void* const* dW, tag_s
 tag_status_t tag_sfb_group_sync(tag_sfb_group_t g, const void* const* X, const void* const* dY,
                                 void* const* dW, tag_stream_t stream) {
     if (!g || !X || !dY || !dW) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync: NULL argument");
-    for (size_t i = 0; i < g->plans.size(); ++i) TAG_TRY(check_ptrs("tag_sfb_group_sync", {dW[i]}));
+    const int count = static_cast<int>(g->plans.size());
+    bool fuse = true;
+    for (int i = 0; i < count; ++i) {
+        TAG_TRY(check_ptrs("tag_sfb_group_sync", {X[i], dY[i], dW[i]}));
+        fuse = fuse && fusable(g->plans[i], dW[i]);
+    }
+    if (fuse) {
+        TAG_TRY(set_device(g->plans[0]->comm));
+        TAG_TRY(check_async(g->plans[0]->comm));
+        return fused_sync(g->plans.data(), count, X, dY, dW, false, nullptr, nullptr,
+                          reinterpret_cast<cudaStream_t>(stream));
+    }
     TAG_TRY(tag_sfb_group_gather(g, X, dY, stream));
     return tag_sfb_group_reconstruct(g, dW, stream);
 }

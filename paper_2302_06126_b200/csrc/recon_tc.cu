@@ -30,6 +30,9 @@
 #include <cstring>
 #include <mutex>
 
+#include <nccl.h>
+#include <nccl_device.h>
+
 #include "ptx.cuh"
 #include "tag_internal.h"
 
@@ -73,6 +76,13 @@ struct LayerParams {
     int num_n_blocks, num_k_blocks;
     int tile_begin;   // first global tile index of this layer
     float alpha;
+    // fused all-gather (FUSED = true): this rank's factors are pushed into every peer's window
+    const void* srcX;      // X_r (B x M, wire dtype)
+    const void* srcY;      // dY_r (B x N)
+    ncclWindow_t win;      // the layer's symmetric window
+    uint64_t off_x, off_dy, off_flag;   // this call's X_all / dY_all buffer and arrival counter
+    int64_t vx, vy;        // 16-byte vectors of X_r / dY_r
+    uint32_t flag_target;  // arrival count that means "every rank's factors have landed"
 };
 
 struct GroupParams {
@@ -80,6 +90,7 @@ struct GroupParams {
     int count;
     int num_tiles;
     float lr, mu, wd;
+    int slot;              // this rank (its slot in X_all / dY_all)
 };
 
 struct TileRef {
@@ -107,9 +118,64 @@ __device__ __forceinline__ void grid_dep_launch() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-template <int BN, bool OUT_BF16, bool SGD>
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Fused all-gather (a1 + a2 inside the reconstruction kernel). Every CTA pushes an even slice of
+// every layer's local factors into slot `rank` of every peer's window (NVLink stores through
+// the NCCL LSA mapping; peer order rotated by rank), then — after a CTA barrier — one thread
+// publishes the slice with a release-add at system scope on every peer's per-layer arrival
+// counter. Layers are pushed in bucket order, so layer 0 is complete first and its tiles can be
+// reconstructed while later layers are still in flight on NVLink.
+__device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, int me) {
+    const int64_t G = gridDim.x;
+    for (int li = 0; li < gp.count; ++li) {
+        const LayerParams& L = gp.L[li];
+        const int64_t V = L.vx + L.vy;
+        const int64_t beg = V * blockIdx.x / G, end = V * (blockIdx.x + 1) / G;
+        for (int64_t v = beg + threadIdx.x; v < end; v += blockDim.x) {
+            const bool isx = v < L.vx;
+            const int64_t i = isx ? v : v - L.vx;
+            const uint4 val = __ldcs(reinterpret_cast<const uint4*>(isx ? L.srcX : L.srcY) + i);
+            const size_t off = isx ? L.off_x + (static_cast<size_t>(gp.slot) * L.vx + i) * 16
+                                   : L.off_dy + (static_cast<size_t>(gp.slot) * L.vy + i) * 16;
+            for (int k = 0; k < npeers; ++k) {
+                const int p = (me + k) % npeers;
+                *reinterpret_cast<uint4*>(ncclGetLsaPointer(L.win, off, p)) = val;
+            }
+        }
+        __syncthreads();                  // the whole CTA's slice of layer li is written
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < npeers; ++k) {
+                const int p = (me + k) % npeers;
+                uint32_t* ctr = static_cast<uint32_t*>(ncclGetLsaPointer(L.win, L.off_flag, p));
+                asm volatile("red.release.sys.global.add.u32 [%0], 1;"
+                             :: "l"(ctr) : "memory");
+            }
+        }
+    }
+}
+
+// Producer side: wait until every rank's every CTA has published layer li (acquire, system
+// scope), then order those generic-proxy writes before the async-proxy (TMA) reads.
+__device__ __forceinline__ void fused_wait(const LayerParams& L, int me) {
+    const uint32_t* ctr = static_cast<const uint32_t*>(ncclGetLsaPointer(L.win, L.off_flag, me));
+    const uint64_t t0 = gtimer();
+    while (true) {
+        uint32_t got;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(got) : "l"(ctr) : "memory");
+        if (static_cast<int32_t>(got - L.flag_target) >= 0) break;
+        if (gtimer() - t0 > 10ull * 1000 * 1000 * 1000) __trap();   // a peer never arrived (10 s)
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+template <int BN, bool OUT_BF16, bool SGD, bool FUSED>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-recon_tc_kernel(const __grid_constant__ GroupParams gp)
+recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const int me)
 {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
@@ -153,14 +219,22 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp)
     const uint32_t tmem_base = *tmem_slot_ptr;
     // no global memory is touched before the previous grid in the stream has completed
     grid_dep_wait();
+    if constexpr (FUSED) fused_push(gp, npeers, me);
 
     if (warp == 0) {
         // ===================================================== TMA producer
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            uint32_t ready = 0;               // FUSED: layers whose factors have all landed
             for (int tile = blockIdx.x; tile < gp.num_tiles; tile += gridDim.x) {
                 const TileRef tr = locate<BN>(gp, tile);
+                if constexpr (FUSED) {
+                    if (!(ready & (1u << tr.li))) {
+                        fused_wait(gp.L[tr.li], me);
+                        ready |= 1u << tr.li;
+                    }
+                }
                 const CUtensorMap* tmA = &gp.L[tr.li].tmA;
                 const CUtensorMap* tmB = &gp.L[tr.li].tmB;
                 const int nkb = gp.L[tr.li].num_k_blocks;
@@ -384,8 +458,26 @@ bool encode_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esiz
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, bool OUT_BF16, bool SGD>
-tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s) {
+int tiles_for(const ReconArgs* a, int count, int bn) {
+    int64_t tiles = 0;
+    for (int i = 0; i < count; ++i) tiles += ((a[i].M + BM - 1) / BM) * ((a[i].N + bn - 1) / bn);
+    return static_cast<int>(tiles);
+}
+
+bool use_wide(const ReconArgs* a, int count) {
+    int64_t kmax = 0;
+    for (int i = 0; i < count; ++i) kmax = a[i].K > kmax ? a[i].K : kmax;
+    // Small K (the HBM-write-bound regime of the paper's small-batch layers): BN = 128 tiles,
+    // 4 TMEM accumulators, finer tail. K >= 192: BN = 256 cuts the A-operand re-reads from L2
+    // (L2 bandwidth binds first there: measured 102 -> 88 us for fc6 at K = 256) and the smem
+    // read rate per MMA (96 instead of 128 B/cycle); 2 accumulators.
+    bool wide = kmax >= 192;
+    if (const char* e = std::getenv("TAG_RECON_BN")) wide = std::atoi(e) == 256;   // experiments
+    return wide;
+}
+
+template <int BN, bool OUT_BF16, bool SGD, bool FUSED>
+tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
     using C = Cfg<BN>;
     GroupParams gp;
     std::memset(&gp, 0, sizeof gp);
@@ -405,13 +497,25 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s) {
         L.tile_begin = tiles;
         L.alpha = a[i].alpha;
         tiles += static_cast<int>((a[i].M + BM - 1) / BM) * L.num_n_blocks;
+        if constexpr (FUSED) {
+            L.srcX = a[i].srcX;
+            L.srcY = a[i].srcY;
+            L.win = static_cast<ncclWindow_t>(a[i].win);
+            L.off_x = a[i].off_x;
+            L.off_dy = a[i].off_dy;
+            L.off_flag = a[i].off_flag;
+            L.vx = a[i].cx * 2 / 16;
+            L.vy = a[i].cy * 2 / 16;
+            L.flag_target = a[i].flag_target;
+        }
     }
     gp.count = count;
     gp.num_tiles = tiles;
     gp.lr = a[0].lr;
     gp.mu = a[0].mu;
     gp.wd = a[0].wd;
-    auto kern = recon_tc_kernel<BN, OUT_BF16, SGD>;
+    gp.slot = FUSED ? fg->me : 0;
+    auto kern = recon_tc_kernel<BN, OUT_BF16, SGD, FUSED>;
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -429,10 +533,24 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, gp);
+    const int npeers = FUSED ? fg->npeers : 1, me = FUSED ? fg->me : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, gp, npeers, me);
     if (e != cudaSuccess) return cuda_fail(e, "launch recon_tc_kernel");
     count_launch();
     return TAG_OK;
+}
+
+template <bool FUSED>
+tag_status_t dispatch(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
+    const bool wide = use_wide(a, count);
+    if (a[0].sgd)
+        return wide ? launch_t<256, false, true, FUSED>(a, count, s, fg)
+                    : launch_t<128, false, true, FUSED>(a, count, s, fg);
+    if (a[0].out == TAG_BF16)
+        return wide ? launch_t<256, true, false, FUSED>(a, count, s, fg)
+                    : launch_t<128, true, false, FUSED>(a, count, s, fg);
+    return wide ? launch_t<256, false, false, FUSED>(a, count, s, fg)
+                : launch_t<128, false, false, FUSED>(a, count, s, fg);
 }
 
 }  // namespace
@@ -450,24 +568,18 @@ bool recon_tc_ok(const ReconArgs& a) {
     return true;
 }
 
-tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s) {
+int recon_tc_grid(const ReconArgs* a, int count) {
+    const int tiles = tiles_for(a, count, use_wide(a, count) ? 256 : 128);
+    return tiles < num_sms() ? tiles : num_sms();
+}
+
+tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s,
+                                   const FusedGather* fused) {
     if (count < 1 || count > MAX_GROUP) return fail(TAG_ERR_INVALID_ARG, "recon group size");
-    int64_t kmax = 0;
-    for (int i = 0; i < count; ++i) {
+    for (int i = 0; i < count; ++i)
         if (a[i].sgd != a[0].sgd || a[i].out != a[0].out)
             return fail(TAG_ERR_INVALID_ARG, "recon group: mixed epilogues");
-        kmax = a[i].K > kmax ? a[i].K : kmax;
-    }
-    // Small K (the HBM-write-bound regime of the paper's small-batch layers): BN = 128 tiles,
-    // 4 TMEM accumulators, finer tail. K >= 192: BN = 256 cuts the A-operand re-reads from L2
-    // (L2 bandwidth binds first there: measured 102 -> 88 us for fc6 at K = 256) and the smem
-    // read rate per MMA (96 instead of 128 B/cycle); 2 accumulators.
-    bool wide = kmax >= 192;
-    if (const char* e = std::getenv("TAG_RECON_BN")) wide = std::atoi(e) == 256;   // experiments
-    if (a[0].sgd) return wide ? launch_t<256, false, true>(a, count, s) : launch_t<128, false, true>(a, count, s);
-    if (a[0].out == TAG_BF16)
-        return wide ? launch_t<256, true, false>(a, count, s) : launch_t<128, true, false>(a, count, s);
-    return wide ? launch_t<256, false, false>(a, count, s) : launch_t<128, false, false>(a, count, s);
+    return fused ? dispatch<true>(a, count, s, fused) : dispatch<false>(a, count, s, nullptr);
 }
 
 tag_status_t launch_recon_tc(const ReconArgs& a, cudaStream_t s) {

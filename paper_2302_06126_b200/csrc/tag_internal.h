@@ -38,6 +38,18 @@ struct ReconArgs {
     float* W;
     float* V;
     float lr, mu, wd;
+    // fused NVLink all-gather (push of this rank's factors inside the reconstruction kernel)
+    const void* srcX;      // X_r, dY_r (wire dtype == in dtype)
+    const void* srcY;
+    void* win;             // ncclWindow_t of the layer's symmetric window
+    uint64_t off_x, off_dy, off_flag;
+    int64_t cx, cy;        // elements of X_r / dY_r
+    uint32_t flag_target;  // arrival-counter value meaning "all ranks' factors landed"
+};
+
+struct FusedGather {
+    int npeers;            // LSA team size (== comm size)
+    int me;                // LSA rank (== comm rank)
 };
 
 // Tensor-core path (tcgen05 + TMEM + TMA). Requires 16-byte aligned rows (see recon_tc_ok).
@@ -45,7 +57,11 @@ bool recon_tc_ok(const ReconArgs& a);
 tag_status_t launch_recon_tc(const ReconArgs& a, cudaStream_t s);
 // Grouped form: one persistent launch over all layers' tiles (1 <= count <= MAX_GROUP).
 constexpr int MAX_GROUP = 8;
-tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s);
+// fused != nullptr: the kernel also pushes this rank's factors to every peer and waits per layer
+// on the arrival counters (see recon_tc.cu). recon_tc_grid: the CTA count such a launch uses.
+tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s,
+                                   const FusedGather* fused = nullptr);
+int recon_tc_grid(const ReconArgs* a, int count);
 // SIMT FFMA path: any shape, fp32 or bf16 operands (exact fp32 accumulation in k order).
 tag_status_t launch_recon_simt(const ReconArgs& a, cudaStream_t s);
 
