@@ -271,9 +271,9 @@ def main():
             # so the interval measures device time, not Python launch latency
             torch.cuda._sleep(SPIN_CYCLES)
             if n > 1:
-                # device-side barrier (1-element NCCL all-reduce, ordered before the start event)
-                # so the inter-process launch skew is not timed as gather latency
-                dist.all_reduce(sync_tok)
+                # device-side barrier of all ranks on this stream (libtag's LSA barrier kernel),
+                # ordered before the start event, so inter-process launch skew is not timed
+                comm.barrier(stream)
         evs[0].record(stream)
         return evs
 

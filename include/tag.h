@@ -97,6 +97,11 @@ tag_status_t tag_comm_create(const unsigned char id[128], int nranks, int rank, 
 /* COLLECTIVE. Destroys the communicator. NULL is a no-op. */
 tag_status_t tag_comm_destroy(tag_comm_t comm);
 tag_status_t tag_comm_info(tag_comm_t comm, int* nranks, int* rank, int* cuda_device);
+/* COLLECTIVE. Stream-ordered device-side barrier of all ranks (one-CTA kernel on the NCCL LSA
+ * barrier): work enqueued on `stream` after it starts only once every rank's stream reached it.
+ * No-op for nranks == 1; TAG_ERR_UNSUPPORTED if the ranks are not all NVLink load/store
+ * reachable. Used to align ranks before a timed region. */
+tag_status_t tag_comm_barrier(tag_comm_t comm, tag_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------ */
 /* SFB plan: one replicated Dense layer                                                       */

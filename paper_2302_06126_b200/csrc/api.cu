@@ -20,7 +20,9 @@ namespace tag {
 tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, void** out);
 void push_devcomm_destroy(ncclComm_t comm, void* dc);
 bool push_devcomm_all_lsa(const void* dc, int nranks);
+tag_status_t launch_comm_barrier(const void* dc, int index, cudaStream_t s);
 constexpr int PUSH_MAX_CTAS = 148;
+constexpr int COMM_BARRIER_INDEX = PUSH_MAX_CTAS;   // LSA barrier slot of tag_comm_barrier
 
 std::atomic<uint64_t> g_launches{0};
 static thread_local std::string t_last_error;
@@ -377,7 +379,7 @@ tag_status_t tag_comm_create(const unsigned char id[128], int nranks, int rank, 
             return nccl_fail(r, "ncclCommInitRank");
         }
         // device API for the NVLink push gather; without it plans use ncclAllGather
-        if (push_devcomm_create(c->nccl, PUSH_MAX_CTAS, &c->devcomm) == TAG_OK)
+        if (push_devcomm_create(c->nccl, PUSH_MAX_CTAS + 1, &c->devcomm) == TAG_OK)
             c->lsa_all = push_devcomm_all_lsa(c->devcomm, nranks);
         else
             c->devcomm = nullptr;
@@ -397,6 +399,16 @@ tag_status_t tag_comm_destroy(tag_comm_t c) {
     }
     delete c;
     return st;
+}
+
+tag_status_t tag_comm_barrier(tag_comm_t c, tag_stream_t stream) {
+    if (!c) return fail(TAG_ERR_INVALID_ARG, "tag_comm_barrier: NULL comm");
+    if (c->nranks == 1) return TAG_OK;
+    TAG_TRY(set_device(c));
+    TAG_TRY(check_async(c));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (c->devcomm && c->lsa_all) return launch_comm_barrier(c->devcomm, COMM_BARRIER_INDEX, s);
+    return fail(TAG_ERR_UNSUPPORTED, "tag_comm_barrier: needs every rank in one NVLink domain");
 }
 
 tag_status_t tag_comm_info(tag_comm_t c, int* nranks, int* rank, int* cuda_device) {

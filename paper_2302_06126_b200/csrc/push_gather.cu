@@ -113,7 +113,21 @@ push_gather_kernel(const ncclDevComm comm, const __grid_constant__ PushGroup g)
     }
 }
 
+// Device-side barrier of the whole comm on a stream (one CTA, LSA barrier index `index`).
+__global__ void comm_barrier_kernel(const ncclDevComm comm, int index) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), index);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
 }  // namespace
+
+tag_status_t launch_comm_barrier(const void* dc, int index, cudaStream_t s) {
+    comm_barrier_kernel<<<1, 32, 0, s>>>(*static_cast<const ncclDevComm*>(dc), index);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "launch comm_barrier_kernel");
+    count_launch();
+    return TAG_OK;
+}
 
 tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, void** out) {
     ncclDevCommRequirements reqs;

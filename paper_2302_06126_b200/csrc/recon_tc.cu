@@ -47,20 +47,23 @@ constexpr int CHUNK_BYTES = BK * 128;    // one 128-byte-wide MN chunk of BK row
 constexpr int EPI_BUF_BYTES = 2 * 32 * 128;  // 2 x (32 rows x 128 B) transpose buffers per warp
 constexpr int TMEM_COLS = 512;
 
-template <int BN>
+// CTAS = 2: a CTA pair on one TPC runs tcgen05 cta_group::2 — UMMA M = 256 (128 rows of A in
+// each CTA's smem), N = BN (BN/2 columns of B in each CTA's smem), each CTA's TMEM holds its
+// 128 rows x BN fp32 accumulator. Halves the per-SM smem operand traffic and the L2 re-reads of B.
+template <int BN, int CTAS>
 struct Cfg {
     static constexpr int ACC = TMEM_COLS / BN;            // accumulator buffers in TMEM
     static constexpr int A_BYTES = (BM / 64) * CHUNK_BYTES;
-    static constexpr int B_BYTES = (BN / 64) * CHUNK_BYTES;
+    static constexpr int B_BYTES = (BN / CTAS / 64) * CHUNK_BYTES;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int STAGES = BN == 256 ? 6 : 8;
     static constexpr int EPI_BYTES = NUM_EPI_WARPS * EPI_BUF_BYTES;
     static constexpr int BAR_BYTES = 256;
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
-    // kind::f16 instruction descriptor: D f32, A/B bf16, both MN-major, N = BN, M = 128.
+    // kind::f16 instruction descriptor: D f32, A/B bf16, both MN-major, N = BN, M = 128 * CTAS.
     static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
                                       (1u << 16) | (uint32_t(BN >> 3) << 17) |
-                                      (uint32_t(BM >> 4) << 24);
+                                      (uint32_t((BM * CTAS) >> 4) << 24);
 };
 
 // One launch reconstructs a group of layers (a gradient bucket): their output tiles are
@@ -97,13 +100,14 @@ struct TileRef {
     int li, m0, n0;
 };
 
-template <int BN>
+// m0 is the first row of the (BM * CTAS)-row tile; CTA rank r of a pair owns rows m0 + r * BM.
+template <int BN, int CTAS>
 __device__ __forceinline__ TileRef locate(const GroupParams& gp, int tile) {
     int li = 0;
     while (li + 1 < gp.count && tile >= gp.L[li + 1].tile_begin) ++li;
     const int t = tile - gp.L[li].tile_begin;
     const int nnb = gp.L[li].num_n_blocks;
-    return TileRef{li, (t / nnb) * BM, (t % nnb) * BN};
+    return TileRef{li, (t / nnb) * BM * CTAS, (t % nnb) * BN};
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -127,33 +131,48 @@ __device__ __forceinline__ uint64_t gtimer() {
 // Fused all-gather (a1 + a2 inside the reconstruction kernel). Every CTA pushes an even slice of
 // every layer's local factors into slot `rank` of every peer's window (NVLink stores through
 // the NCCL LSA mapping; peer order rotated by rank), then — after a CTA barrier — one thread
-// publishes the slice with a release-add at system scope on every peer's per-layer arrival
-// counter. Layers are pushed in bucket order, so layer 0 is complete first and its tiles can be
-// reconstructed while later layers are still in flight on NVLink.
+// issues one system-scope fence and adds 1 to every layer's arrival counter on every peer. The
+// TMA producer of each CTA waits for a layer's counter before loading that layer's first tile.
 __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, int me) {
     const int64_t G = gridDim.x;
+    constexpr int U = 4;                  // 16-byte loads in flight per thread before the stores
     for (int li = 0; li < gp.count; ++li) {
         const LayerParams& L = gp.L[li];
         const int64_t V = L.vx + L.vy;
         const int64_t beg = V * blockIdx.x / G, end = V * (blockIdx.x + 1) / G;
-        for (int64_t v = beg + threadIdx.x; v < end; v += blockDim.x) {
-            const bool isx = v < L.vx;
-            const int64_t i = isx ? v : v - L.vx;
-            const uint4 val = __ldcs(reinterpret_cast<const uint4*>(isx ? L.srcX : L.srcY) + i);
-            const size_t off = isx ? L.off_x + (static_cast<size_t>(gp.slot) * L.vx + i) * 16
-                                   : L.off_dy + (static_cast<size_t>(gp.slot) * L.vy + i) * 16;
-            for (int k = 0; k < npeers; ++k) {
-                const int p = (me + k) % npeers;
-                *reinterpret_cast<uint4*>(ncclGetLsaPointer(L.win, off, p)) = val;
+        for (int64_t v0 = beg + threadIdx.x; v0 < end; v0 += U * static_cast<int64_t>(blockDim.x)) {
+            uint4 val[U];
+            size_t off[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t v = v0 + u * static_cast<int64_t>(blockDim.x);
+                if (v >= end) break;
+                const bool isx = v < L.vx;
+                const int64_t i = isx ? v : v - L.vx;
+                val[u] = __ldcs(reinterpret_cast<const uint4*>(isx ? L.srcX : L.srcY) + i);
+                off[u] = isx ? L.off_x + (static_cast<size_t>(gp.slot) * L.vx + i) * 16
+                             : L.off_dy + (static_cast<size_t>(gp.slot) * L.vy + i) * 16;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (v0 + u * static_cast<int64_t>(blockDim.x) >= end) break;
+                for (int k = 0; k < npeers; ++k) {
+                    const int p = (me + k) % npeers;
+                    *reinterpret_cast<uint4*>(ncclGetLsaPointer(L.win, off[u], p)) = val[u];
+                }
             }
         }
-        __syncthreads();                  // the whole CTA's slice of layer li is written
-        if (threadIdx.x == 0) {
+    }
+    // One system-scope release for the whole slice (a fence per layer costs a NVLink round trip
+    // each), then relaxed increments of every layer's arrival counter on every peer.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        for (int li = 0; li < gp.count; ++li) {
             for (int k = 0; k < npeers; ++k) {
                 const int p = (me + k) % npeers;
-                uint32_t* ctr = static_cast<uint32_t*>(ncclGetLsaPointer(L.win, L.off_flag, p));
-                asm volatile("red.release.sys.global.add.u32 [%0], 1;"
-                             :: "l"(ctr) : "memory");
+                uint32_t* ctr = static_cast<uint32_t*>(ncclGetLsaPointer(gp.L[li].win, gp.L[li].off_flag, p));
+                asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" :: "l"(ctr) : "memory");
             }
         }
     }
@@ -173,11 +192,11 @@ __device__ __forceinline__ void fused_wait(const LayerParams& L, int me) {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-template <int BN, bool OUT_BF16, bool SGD, bool FUSED>
+template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const int me)
 {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, CTAS>;
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the SWIZZLE_128B atoms
     const uint32_t base = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -195,6 +214,9 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
 
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
+    const uint32_t crank = CTAS == 2 ? ptx::cluster_ctarank() : 0;   // 0 = leader of the pair
+    const int unit = blockIdx.x / CTAS;      // this CTA's (pair's) index in the tile schedule
+    const int nunits = gridDim.x / CTAS;
 
     // ---- prologue (overlaps the previous kernel's tail under programmatic dependent launch)
     if (warp == 0 && lane == 0) {
@@ -203,18 +225,22 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
             ptx::tma_prefetch_desc(&gp.L[i].tmB);
         }
         for (int s = 0; s < C::STAGES; ++s) {
-            ptx::mbar_init(bar_full + 8 * s, 1);
+            ptx::mbar_init(bar_full + 8 * s, CTAS);      // pair: the leader's, armed by both
             ptx::mbar_init(bar_empty + 8 * s, 1);
         }
         for (int a = 0; a < C::ACC; ++a) {
             ptx::mbar_init(bar_tfull + 8 * a, 1);
-            ptx::mbar_init(bar_tempty + 8 * a, NUM_EPI_WARPS);
+            ptx::mbar_init(bar_tempty + 8 * a, NUM_EPI_WARPS * CTAS);   // pair: both CTAs drain
         }
         ptx::fence_mbar_init();
     }
-    if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(s_tmem_slot);
+    if (warp == 1) {
+        if constexpr (CTAS == 2) ptx::tmem_alloc_cg2<TMEM_COLS>(s_tmem_slot);
+        else ptx::tmem_alloc<TMEM_COLS>(s_tmem_slot);
+    }
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CTAS == 2) ptx::cluster_sync();
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot_ptr;
     // no global memory is touched before the previous grid in the stream has completed
@@ -227,8 +253,8 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
             int stage = 0;
             uint32_t phase = 0;
             uint32_t ready = 0;               // FUSED: layers whose factors have all landed
-            for (int tile = blockIdx.x; tile < gp.num_tiles; tile += gridDim.x) {
-                const TileRef tr = locate<BN>(gp, tile);
+            for (int tile = unit; tile < gp.num_tiles; tile += nunits) {
+                const TileRef tr = locate<BN, CTAS>(gp, tile);
                 if constexpr (FUSED) {
                     if (!(ready & (1u << tr.li))) {
                         fused_wait(gp.L[tr.li], me);
@@ -241,28 +267,45 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                 for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait(bar_empty + 8 * stage, phase ^ 1);
                     const uint32_t fb = bar_full + 8 * stage;
-                    ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
                     const uint32_t sa = s_stages + stage * C::STAGE_BYTES;
                     const uint32_t sb = sa + C::A_BYTES;
+                    const int am0 = tr.m0 + static_cast<int>(crank) * BM;          // my A rows
+                    const int bn0 = tr.n0 + static_cast<int>(crank) * (BN / CTAS); // my B cols
+                    if constexpr (CTAS == 2) {
+                        // both halves land on the leader's barrier, which the leader arms for
+                        // the pair's bytes; the peer adds its arrival (count 2)
+                        const uint32_t fbl = ptx::mapa(fb, 0);
+                        if (crank == 0) ptx::mbar_arrive_expect_tx(fb, CTAS * C::STAGE_BYTES);
+                        else ptx::mbar_arrive_cluster(fbl);
 #pragma unroll
-                    for (int c = 0; c < BM / 64; ++c)
-                        ptx::tma_load_2d(sa + c * CHUNK_BYTES, tmA, fb, tr.m0 + 64 * c, kb * BK);
+                        for (int c = 0; c < BM / 64; ++c)
+                            ptx::tma_load_2d_cg2(sa + c * CHUNK_BYTES, tmA, fbl, am0 + 64 * c, kb * BK);
 #pragma unroll
-                    for (int c = 0; c < BN / 64; ++c)
-                        ptx::tma_load_2d(sb + c * CHUNK_BYTES, tmB, fb, tr.n0 + 64 * c, kb * BK);
+                        for (int c = 0; c < BN / CTAS / 64; ++c)
+                            ptx::tma_load_2d_cg2(sb + c * CHUNK_BYTES, tmB, fbl, bn0 + 64 * c, kb * BK);
+                    } else {
+                        ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+#pragma unroll
+                        for (int c = 0; c < BM / 64; ++c)
+                            ptx::tma_load_2d(sa + c * CHUNK_BYTES, tmA, fb, am0 + 64 * c, kb * BK);
+#pragma unroll
+                        for (int c = 0; c < BN / 64; ++c)
+                            ptx::tma_load_2d(sb + c * CHUNK_BYTES, tmB, fb, bn0 + 64 * c, kb * BK);
+                    }
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ===================================================== MMA issuer (one thread)
-        if (lane == 0) {
+        // ===================================================== MMA issuer (one thread; the
+        // leader CTA's only, for a pair)
+        if (lane == 0 && crank == 0) {
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = blockIdx.x; tile < gp.num_tiles; tile += gridDim.x) {
-                const int nkb = gp.L[locate<BN>(gp, tile).li].num_k_blocks;
+            for (int tile = unit; tile < gp.num_tiles; tile += nunits) {
+                const int nkb = gp.L[locate<BN, CTAS>(gp, tile).li].num_k_blocks;
                 ptx::mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);   // epilogue drained it
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -276,12 +319,17 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                         // 16 K rows = two 8-row swizzle atoms = 2048 bytes per UMMA_K step
                         const uint64_t ad = ptx::sw128_desc(sa + kk * 2048, CHUNK_BYTES, 1024);
                         const uint64_t bd = ptx::sw128_desc(sb + kk * 2048, CHUNK_BYTES, 1024);
-                        ptx::mma_f16(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0);
+                        if constexpr (CTAS == 2) ptx::mma_f16_cg2(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0);
+                        else ptx::mma_f16(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0);
                     }
-                    ptx::mma_commit(bar_empty + 8 * stage);            // frees the smem slot
+                    // frees the smem slot (both CTAs' slots for a pair)
+                    if constexpr (CTAS == 2) ptx::mma_commit_cg2_mc(bar_empty + 8 * stage, 0x3);
+                    else ptx::mma_commit(bar_empty + 8 * stage);
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
-                ptx::mma_commit(bar_tfull + 8 * acc);                   // accumulator ready
+                // accumulator ready (both CTAs' epilogues for a pair)
+                if constexpr (CTAS == 2) ptx::mma_commit_cg2_mc(bar_tfull + 8 * acc, 0x3);
+                else ptx::mma_commit(bar_tfull + 8 * acc);
                 if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
             }
             // all MMAs of this CTA are issued: let the next kernel in the stream start launching
@@ -307,8 +355,9 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
         int acc = 0;
         uint32_t acc_phase = 0;
         const float lr = gp.lr, mu = gp.mu, wd = gp.wd;
-        for (int tile = blockIdx.x; tile < gp.num_tiles; tile += gridDim.x) {
-            const TileRef tr = locate<BN>(gp, tile);
+        const uint32_t tempty_leader = CTAS == 2 ? ptx::mapa(bar_tempty, 0) : bar_tempty;
+        for (int tile = unit; tile < gp.num_tiles; tile += nunits) {
+            const TileRef tr = locate<BN, CTAS>(gp, tile);
             // this tile's layer parameters, read once into registers
             const LayerParams& lp = gp.L[tr.li];
             uint8_t* const Cp = static_cast<uint8_t*>(lp.C);
@@ -317,7 +366,7 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
             const int M = lp.M, N = lp.N;
             const float alpha = lp.alpha;
             const int n0 = tr.n0;
-            const int row0 = tr.m0 + 32 * quad;  // first output row of this warp
+            const int row0 = tr.m0 + static_cast<int>(crank) * BM + 32 * quad;  // first row
             ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
             ptx::tc_fence_after();
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quad) << 16) + acc * BN;
@@ -327,7 +376,10 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
             if (nch == 0) {                       // nothing to read: release the accumulator
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+                if (lane == 0) {
+                    if constexpr (CTAS == 2) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
+                    else ptx::mbar_arrive(bar_tempty + 8 * acc);
+                }
             }
 #pragma unroll 1
             for (int ch = 0; ch < nch; ch += PAIR) {
@@ -366,7 +418,10 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                     // last TMEM read of this accumulator by this warp: hand it back to the MMA
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(bar_tempty + 8 * acc);
+                    if (lane == 0) {
+                    if constexpr (CTAS == 2) ptx::mbar_arrive_cluster(tempty_leader + 8 * acc);
+                    else ptx::mbar_arrive(bar_tempty + 8 * acc);
+                }
                 }
                 // ---- registers -> 128B-swizzled smem (row `lane`), conflict-free
                 __syncwarp();                     // previous round's smem reads are done
@@ -424,9 +479,13 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CTAS == 2) ptx::cluster_sync();   // the leader's MMAs into the peer are done
+    else __syncthreads();
     ptx::tc_fence_after();
-    if (warp == 1) ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+    if (warp == 1) {
+        if constexpr (CTAS == 2) ptx::tmem_dealloc_cg2<TMEM_COLS>(tmem_base);
+        else ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
 }
 
 // ------------------------------------------------------------------ host side
@@ -458,9 +517,10 @@ bool encode_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esiz
     return r == CUDA_SUCCESS;
 }
 
-int tiles_for(const ReconArgs* a, int count, int bn) {
+int tiles_for(const ReconArgs* a, int count, int bn, int ctas) {
     int64_t tiles = 0;
-    for (int i = 0; i < count; ++i) tiles += ((a[i].M + BM - 1) / BM) * ((a[i].N + bn - 1) / bn);
+    for (int i = 0; i < count; ++i)
+        tiles += ((a[i].M + BM * ctas - 1) / (BM * ctas)) * ((a[i].N + bn - 1) / bn);
     return static_cast<int>(tiles);
 }
 
@@ -468,17 +528,23 @@ bool use_wide(const ReconArgs* a, int count) {
     int64_t kmax = 0;
     for (int i = 0; i < count; ++i) kmax = a[i].K > kmax ? a[i].K : kmax;
     // Small K (the HBM-write-bound regime of the paper's small-batch layers): BN = 128 tiles,
-    // 4 TMEM accumulators, finer tail. K >= 192: BN = 256 cuts the A-operand re-reads from L2
-    // (L2 bandwidth binds first there: measured 102 -> 88 us for fc6 at K = 256) and the smem
-    // read rate per MMA (96 instead of 128 B/cycle); 2 accumulators.
+    // 4 TMEM accumulators, finer tail. K >= 192: BN = 256 on a CTA pair (cta_group::2, 256 x 256
+    // tiles): the operand re-reads from L2 bind first there (fc6 at K = 256, one CTA: 102 us at
+    // BN = 128, 88 us at BN = 256 with L2 throughput saturated), and the pair halves them again.
     bool wide = kmax >= 192;
     if (const char* e = std::getenv("TAG_RECON_BN")) wide = std::atoi(e) == 256;   // experiments
     return wide;
 }
 
-template <int BN, bool OUT_BF16, bool SGD, bool FUSED>
+int use_ctas(const ReconArgs* a, int count) {
+    if (!use_wide(a, count)) return 1;
+    if (const char* e = std::getenv("TAG_RECON_CTAS")) return std::atoi(e) == 1 ? 1 : 2;
+    return 2;
+}
+
+template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED>
 tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
-    using C = Cfg<BN>;
+    using C = Cfg<BN, CTAS>;
     GroupParams gp;
     std::memset(&gp, 0, sizeof gp);
     int tiles = 0;
@@ -496,7 +562,7 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
         L.num_k_blocks = static_cast<int>((a[i].K + BK - 1) / BK);
         L.tile_begin = tiles;
         L.alpha = a[i].alpha;
-        tiles += static_cast<int>((a[i].M + BM - 1) / BM) * L.num_n_blocks;
+        tiles += static_cast<int>((a[i].M + BM * CTAS - 1) / (BM * CTAS)) * L.num_n_blocks;
         if constexpr (FUSED) {
             L.srcX = a[i].srcX;
             L.srcY = a[i].srcY;
@@ -515,7 +581,7 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     gp.mu = a[0].mu;
     gp.wd = a[0].wd;
     gp.slot = FUSED ? fg->me : 0;
-    auto kern = recon_tc_kernel<BN, OUT_BF16, SGD, FUSED>;
+    auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED>;
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -523,16 +589,21 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recon_tc)");
         attr_set = true;
     }
+    const int units = num_sms() / CTAS;     // one CTA (pair) per SM (TPC)
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(tiles < num_sms() ? tiles : num_sms()));
+    cfg.gridDim = dim3(static_cast<unsigned>(CTAS * (tiles < units ? tiles : units)));
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see kernel)
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;                  // CTA pair on one TPC
+    attr[1].val.clusterDim.x = CTAS;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = CTAS == 2 ? 2 : 1;
     const int npeers = FUSED ? fg->npeers : 1, me = FUSED ? fg->me : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, gp, npeers, me);
     if (e != cudaSuccess) return cuda_fail(e, "launch recon_tc_kernel");
@@ -543,14 +614,20 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
 template <bool FUSED>
 tag_status_t dispatch(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
     const bool wide = use_wide(a, count);
-    if (a[0].sgd)
-        return wide ? launch_t<256, false, true, FUSED>(a, count, s, fg)
-                    : launch_t<128, false, true, FUSED>(a, count, s, fg);
-    if (a[0].out == TAG_BF16)
-        return wide ? launch_t<256, true, false, FUSED>(a, count, s, fg)
-                    : launch_t<128, true, false, FUSED>(a, count, s, fg);
-    return wide ? launch_t<256, false, false, FUSED>(a, count, s, fg)
-                : launch_t<128, false, false, FUSED>(a, count, s, fg);
+    const bool pair = use_ctas(a, count) == 2;
+    if (a[0].sgd) {
+        if (!wide) return launch_t<128, 1, false, true, FUSED>(a, count, s, fg);
+        return pair ? launch_t<256, 2, false, true, FUSED>(a, count, s, fg)
+                    : launch_t<256, 1, false, true, FUSED>(a, count, s, fg);
+    }
+    if (a[0].out == TAG_BF16) {
+        if (!wide) return launch_t<128, 1, true, false, FUSED>(a, count, s, fg);
+        return pair ? launch_t<256, 2, true, false, FUSED>(a, count, s, fg)
+                    : launch_t<256, 1, true, false, FUSED>(a, count, s, fg);
+    }
+    if (!wide) return launch_t<128, 1, false, false, FUSED>(a, count, s, fg);
+    return pair ? launch_t<256, 2, false, false, FUSED>(a, count, s, fg)
+                : launch_t<256, 1, false, false, FUSED>(a, count, s, fg);
 }
 
 }  // namespace
@@ -569,8 +646,10 @@ bool recon_tc_ok(const ReconArgs& a) {
 }
 
 int recon_tc_grid(const ReconArgs* a, int count) {
-    const int tiles = tiles_for(a, count, use_wide(a, count) ? 256 : 128);
-    return tiles < num_sms() ? tiles : num_sms();
+    const int ctas = use_ctas(a, count);
+    const int tiles = tiles_for(a, count, use_wide(a, count) ? 256 : 128, ctas);
+    const int units = num_sms() / ctas;
+    return ctas * (tiles < units ? tiles : units);
 }
 
 tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s,

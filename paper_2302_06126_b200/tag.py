@@ -65,6 +65,7 @@ _SIGS = {
     "tag_comm_create": ([ctypes.c_char_p, _i, _i, _i, _p(_vp)], _st),
     "tag_comm_destroy": ([_vp], _st),
     "tag_comm_info": ([_vp, _p(_i), _p(_i), _p(_i)], _st),
+    "tag_comm_barrier": ([_vp, _vp], _st),
     "tag_sfb_plan": ([_vp, _p(SfbDesc), _p(_vp)], _st),
     "tag_sfb_plan_destroy": ([_vp], _st),
     "tag_sfb_plan_info": ([_vp, _p(PlanInfo)], _st),
@@ -160,6 +161,10 @@ class Comm:
     @property
     def handle(self):
         return self._h
+
+    def barrier(self, stream=None):
+        """Stream-ordered device-side barrier of all ranks (no-op for one rank)."""
+        _check(_lib.tag_comm_barrier(self._h, _stream(stream)), "tag_comm_barrier")
 
     def close(self):
         if self._h:
