@@ -37,7 +37,7 @@ import torch.distributed as dist  # noqa: E402
 
 METRIC = "per-layer SFB grad-sync us & dW GB/s (VGG-19 fc6/fc7/fc8, B=32/GPU)"
 ESIZE = {"f32": 4, "bf16": 2}
-SPIN_CYCLES = 80_000   # torch.cuda._sleep before each start event (not a libtag kernel)
+SPIN_CYCLES = 1_000_000   # ~0.5 ms torch.cuda._sleep before each start event (not a libtag kernel)
 
 
 def load_peaks():
@@ -267,7 +267,7 @@ def main():
         tdist.barrier()
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(k)]
         with torch.cuda.stream(stream):
-            # a ~40 us device spin ahead of the start event lets the host enqueue the whole step,
+            # a ~0.5 ms device spin ahead of the start event lets the host enqueue the whole step,
             # so the interval measures device time, not Python launch latency
             torch.cuda._sleep(SPIN_CYCLES)
             if n > 1:
