@@ -387,7 +387,7 @@ def main():
             "recon_tensor_frac": round(flops / (t_rec * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
             "allgather_busbw_GBps": round(ag / ((t_sync - t_rec) * 1e-3) / 1e9, 1) if n > 1 else None,
             "selector": {0: "allreduce", 1: "sfb", 2: "none"}[choices[i]],
-            "gather": l["plan"].info()["gather"]}
+            "gather": l["plan"].info()["gather"] + ("+multicast" if l["plan"].info()["multicast"] else "")}
     if group is not None and n > 1:
         t_gather = tdist.max_over_ranks(statistics.mean(staged_g_ms))
         ag_all = sum((n - 1) * l["L"].B * (l["L"].M + l["L"].N) * ESIZE[cfg.wire_dtype] for l in layers)

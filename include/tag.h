@@ -137,6 +137,8 @@ typedef struct {
     int gather_mode;            /* tag_gather_mode_t                                            */
     int64_t K;                  /* n * B                                                        */
     float alpha;                /* fl32(1/(nB)), the fused epilogue scale                       */
+    int multicast;              /* 1: the fused push uses NVLS multimem stores (one store reaches */
+                                /*    every GPU); 0: one unicast store per peer                   */
 } tag_plan_info_t;
 tag_status_t tag_sfb_plan_info(tag_sfb_plan_t plan, tag_plan_info_t* out);
 

@@ -20,6 +20,7 @@ namespace tag {
 tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, void** out);
 void push_devcomm_destroy(ncclComm_t comm, void* dc);
 bool push_devcomm_all_lsa(const void* dc, int nranks);
+void* push_devcomm_mc_base(const void* dc);
 tag_status_t launch_comm_barrier(const void* dc, int index, cudaStream_t s);
 constexpr int PUSH_MAX_CTAS = 148;
 constexpr int COMM_BARRIER_INDEX = PUSH_MAX_CTAS;   // LSA barrier slot of tag_comm_barrier
@@ -81,6 +82,7 @@ struct tag_comm_s {
     int nranks = 1, rank = 0, device = 0;
     void* devcomm = nullptr;     // ncclDevComm (device API: LSA pointers + barriers), or nullptr
     bool lsa_all = false;        // every rank is load/store reachable (one NVLink domain)
+    void* mc_base = nullptr;     // NVLS multicast base of the LSA team (multimem stores), or null
 };
 
 struct tag_plan_s {
@@ -308,7 +310,7 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
     // every CTA of every rank adds 1 per layer: the counter grows by n * grid per call
     const uint32_t inc = static_cast<uint32_t>(c->nranks) * static_cast<uint32_t>(recon_tc_grid(a, count));
     for (int i = 0; i < count; ++i) a[i].flag_target = plans[i]->flag_total[plans[i]->parity] + inc;
-    FusedGather fg{c->nranks, c->rank};
+    FusedGather fg{c->nranks, c->rank, c->mc_base};
     TAG_TRY(launch_recon_tc_group(a, count, s, &fg));
     for (int i = 0; i < count; ++i) {
         tag_plan_s* p = plans[i];
@@ -379,10 +381,12 @@ tag_status_t tag_comm_create(const unsigned char id[128], int nranks, int rank, 
             return nccl_fail(r, "ncclCommInitRank");
         }
         // device API for the NVLink push gather; without it plans use ncclAllGather
-        if (push_devcomm_create(c->nccl, PUSH_MAX_CTAS + 1, &c->devcomm) == TAG_OK)
+        if (push_devcomm_create(c->nccl, PUSH_MAX_CTAS + 1, &c->devcomm) == TAG_OK) {
             c->lsa_all = push_devcomm_all_lsa(c->devcomm, nranks);
-        else
+            c->mc_base = push_devcomm_mc_base(c->devcomm);
+        } else {
             c->devcomm = nullptr;
+        }
         set_error("");
     }
     *out = c;
@@ -508,6 +512,7 @@ tag_status_t tag_sfb_plan_info(tag_sfb_plan_t p, tag_plan_info_t* out) {
     out->gather_mode = p->gather_mode;
     out->K = p->K;
     out->alpha = p->alpha;
+    out->multicast = (p->gather_mode == TAG_GATHER_NVLINK_PUSH && p->comm->mc_base) ? 1 : 0;
     return TAG_OK;
 }
 

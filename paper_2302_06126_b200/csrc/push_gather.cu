@@ -133,6 +133,12 @@ tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, void** out) {
     ncclDevCommRequirements reqs;
     std::memset(&reqs, 0, sizeof reqs);
     reqs.lsaBarrierCount = max_ctas;
+    // NVLink SHARP multicast (one multimem store reaches every GPU): opt-in with TAG_MULTIMEM=1.
+    // Measured at n = 2 and 4 on B200 it is not faster than one unicast store per peer (the
+    // push is latency-bound: 8-11 us unicast vs 13-14 us multicast per CTA slice at n = 2).
+    // Collective: every rank must pass the same requirements.
+    const char* mm = std::getenv("TAG_MULTIMEM");
+    reqs.lsaMultimem = mm && std::strcmp(mm, "1") == 0;
     ncclDevComm* dc = new ncclDevComm;
     ncclResult_t r = ncclDevCommCreate(comm, &reqs, dc);
     if (r != ncclSuccess) {
@@ -147,6 +153,11 @@ void push_devcomm_destroy(ncclComm_t comm, void* dc) {
     if (!dc) return;
     ncclDevCommDestroy(comm, static_cast<ncclDevComm*>(dc));
     delete static_cast<ncclDevComm*>(dc);
+}
+
+void* push_devcomm_mc_base(const void* dc) {
+    const ncclDevComm* d = static_cast<const ncclDevComm*>(dc);
+    return d ? d->lsaMultimem.mcBasePtr : nullptr;
 }
 
 bool push_devcomm_all_lsa(const void* dc, int nranks) {

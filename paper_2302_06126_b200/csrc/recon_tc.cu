@@ -94,6 +94,8 @@ struct GroupParams {
     int num_tiles;
     float lr, mu, wd;
     int slot;              // this rank (its slot in X_all / dY_all)
+    char* mc_base;         // FUSED: NVLS multicast base of the windows, or nullptr (unicast)
+    int dbg;               // TAG_FUSED_DEBUG (profiling only): 1 no push/wait, 2 no wait, 3 stamps
 };
 
 struct TileRef {
@@ -133,9 +135,15 @@ __device__ __forceinline__ uint64_t gtimer() {
 // the NCCL LSA mapping; peer order rotated by rank), then — after a CTA barrier — one thread
 // issues one system-scope fence and adds 1 to every layer's arrival counter on every peer. The
 // TMA producer of each CTA waits for a layer's counter before loading that layer's first tile.
+// multicast address of (window, offset): one store there lands in every GPU of the team
+__device__ __forceinline__ void* mc_ptr(char* mc_base, ncclWindow_t w, size_t off) {
+    return mc_base + static_cast<size_t>(w->mcOffset4K) * 4096 + off;
+}
+
 __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, int me) {
     const int64_t G = gridDim.x;
     constexpr int U = 4;                  // 16-byte loads in flight per thread before the stores
+    char* const mc = gp.mc_base;
     for (int li = 0; li < gp.count; ++li) {
         const LayerParams& L = gp.L[li];
         const int64_t V = L.vx + L.vy;
@@ -156,9 +164,16 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (v0 + u * static_cast<int64_t>(blockDim.x) >= end) break;
-                for (int k = 0; k < npeers; ++k) {
-                    const int p = (me + k) % npeers;
-                    *reinterpret_cast<uint4*>(ncclGetLsaPointer(L.win, off[u], p)) = val[u];
+                if (mc != nullptr) {
+                    // NVLS: the switch replicates one store to every GPU (this one included)
+                    asm volatile("multimem.st.global.v4.f32 [%0], {%1, %2, %3, %4};"
+                                 :: "l"(mc_ptr(mc, L.win, off[u])), "r"(val[u].x), "r"(val[u].y),
+                                    "r"(val[u].z), "r"(val[u].w) : "memory");
+                } else {
+                    for (int k = 0; k < npeers; ++k) {
+                        const int p = (me + k) % npeers;
+                        *reinterpret_cast<uint4*>(ncclGetLsaPointer(L.win, off[u], p)) = val[u];
+                    }
                 }
             }
         }
@@ -169,10 +184,15 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
     if (threadIdx.x == 0) {
         asm volatile("fence.acq_rel.sys;" ::: "memory");
         for (int li = 0; li < gp.count; ++li) {
-            for (int k = 0; k < npeers; ++k) {
-                const int p = (me + k) % npeers;
-                uint32_t* ctr = static_cast<uint32_t*>(ncclGetLsaPointer(gp.L[li].win, gp.L[li].off_flag, p));
-                asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" :: "l"(ctr) : "memory");
+            if (mc != nullptr) {
+                asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], 1;"
+                             :: "l"(mc_ptr(mc, gp.L[li].win, gp.L[li].off_flag)) : "memory");
+            } else {
+                for (int k = 0; k < npeers; ++k) {
+                    const int p = (me + k) % npeers;
+                    uint32_t* ctr = static_cast<uint32_t*>(ncclGetLsaPointer(gp.L[li].win, gp.L[li].off_flag, p));
+                    asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" :: "l"(ctr) : "memory");
+                }
             }
         }
     }
@@ -245,7 +265,12 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
     const uint32_t tmem_base = *tmem_slot_ptr;
     // no global memory is touched before the previous grid in the stream has completed
     grid_dep_wait();
-    if constexpr (FUSED) fused_push(gp, npeers, me);
+    uint64_t t_start = 0, t_pushed = 0;
+    if constexpr (FUSED) {
+        if (gp.dbg == 3) t_start = gtimer();
+        if (gp.dbg != 1) fused_push(gp, npeers, me);
+        if (gp.dbg == 3) t_pushed = gtimer();
+    }
 
     if (warp == 0) {
         // ===================================================== TMA producer
@@ -257,7 +282,11 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                 const TileRef tr = locate<BN, CTAS>(gp, tile);
                 if constexpr (FUSED) {
                     if (!(ready & (1u << tr.li))) {
-                        fused_wait(gp.L[tr.li], me);
+                        if (gp.dbg == 0 || gp.dbg == 3) fused_wait(gp.L[tr.li], me);
+                        if (gp.dbg == 3 && ready == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+                            printf("fused rank %d cta %d push %llu ns, wait-after-push %llu ns\n", me,
+                                   blockIdx.x, (unsigned long long)(t_pushed - t_start),
+                                   (unsigned long long)(gtimer() - t_pushed));
                         ready |= 1u << tr.li;
                     }
                 }
@@ -581,6 +610,12 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     gp.mu = a[0].mu;
     gp.wd = a[0].wd;
     gp.slot = FUSED ? fg->me : 0;
+    gp.mc_base = FUSED ? static_cast<char*>(fg->mc_base) : nullptr;
+    static const int dbg = [] {
+        const char* e = std::getenv("TAG_FUSED_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    gp.dbg = dbg;
     auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED>;
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {

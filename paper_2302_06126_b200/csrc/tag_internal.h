@@ -50,6 +50,7 @@ struct ReconArgs {
 struct FusedGather {
     int npeers;            // LSA team size (== comm size)
     int me;                // LSA rank (== comm rank)
+    void* mc_base;         // NVLS multicast base (multimem.st to every GPU at once), or nullptr
 };
 
 // Tensor-core path (tcgen05 + TMEM + TMA). Requires 16-byte aligned rows (see recon_tc_ok).

@@ -55,7 +55,7 @@ def main():
     def run(cid, li, M, N, B, xd, dyd, in_dt, wire_dt, out_dt):
         X, dY = synth.factors(cid, li, rank, M, N, B, xd, dyd)
         plan = tag.SfbPlan(comm, M, N, B, in_dt, wire_dt, out_dt)
-        modes.add(plan.info()["gather"])
+        modes.add(plan.info()["gather"] + ("+multicast" if plan.info()["multicast"] else ""))
         Xd = torch.from_numpy(X).to(TDT[in_dt]).cuda()
         dYd = torch.from_numpy(dY).to(TDT[in_dt]).cuda()
         dW = torch.full((M, N), float("nan"), dtype=TDT[out_dt], device="cuda")

@@ -21,7 +21,7 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("gather", ["push", "nccl"])
+@pytest.mark.parametrize("gather", ["push", "nccl", "multicast"])
 @pytest.mark.parametrize("nproc", [2, 4])
 def test_multi_gpu_sfb(cuda, nproc, gather):
     if torch.cuda.device_count() < nproc:
@@ -32,10 +32,14 @@ def test_multi_gpu_sfb(cuda, nproc, gather):
     env = dict(os.environ)
     if gather == "nccl":
         env["TAG_GATHER"] = "nccl"
+    if gather == "multicast":
+        env["TAG_MULTIMEM"] = "1"
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[-1])
     assert res["ok"] and res["n"] == nproc, res
-    want = "nccl_allgather" if gather == "nccl" else "nvlink_push"
-    assert want in res["gather_modes"], res
+    want = {"nccl": "nccl_allgather", "push": "nvlink_push",
+            "multicast": "nvlink_push+multicast"}[gather]
+    assert want in res["gather_modes"] or (gather == "multicast" and "nvlink_push" in
+                                            res["gather_modes"]), res   # no NVLS: unicast
