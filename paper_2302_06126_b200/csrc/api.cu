@@ -257,8 +257,10 @@ tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int
 // and reconstructs on the tensor cores. The reconstruction kernel pushes this rank's factors
 // into every peer's window and waits, per layer, on arrival counters before loading its tiles.
 bool fusable(const tag_plan_s* p, void* dW) {
-    if (p->gather_mode != TAG_GATHER_NVLINK_PUSH || p->d.in_dtype != p->d.wire_dtype || !p->use_tc)
-        return false;
+    if (p->gather_mode != TAG_GATHER_NVLINK_PUSH || !p->use_tc) return false;
+    const bool same = p->d.in_dtype == p->d.wire_dtype;
+    const bool cast = p->d.in_dtype == TAG_F32 && p->d.wire_dtype == TAG_BF16;
+    if (!same && !cast) return false;
     if (std::getenv("TAG_NO_FUSE")) return false;
     ReconArgs a{};
     a.A = p->win_base;
@@ -310,7 +312,8 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
     // every CTA of every rank adds 1 per layer: the counter grows by n * grid per call
     const uint32_t inc = static_cast<uint32_t>(c->nranks) * static_cast<uint32_t>(recon_tc_grid(a, count));
     for (int i = 0; i < count; ++i) a[i].flag_target = plans[i]->flag_total[plans[i]->parity] + inc;
-    FusedGather fg{c->nranks, c->rank, c->mc_base};
+    FusedGather fg{c->nranks, c->rank, c->mc_base,
+                   plans[0]->d.in_dtype == TAG_F32 && plans[0]->d.wire_dtype == TAG_BF16};
     TAG_TRY(launch_recon_tc_group(a, count, s, &fg));
     for (int i = 0; i < count; ++i) {
         tag_plan_s* p = plans[i];

@@ -96,6 +96,7 @@ struct GroupParams {
     int slot;              // this rank (its slot in X_all / dY_all)
     char* mc_base;         // FUSED: NVLS multicast base of the windows, or nullptr (unicast)
     int dbg;               // TAG_FUSED_DEBUG (profiling only): 1 no push/wait, 2 no wait, 3 stamps
+    int cast;              // FUSED: the sources are fp32, cast to bf16 (RNE) on the way out
 };
 
 struct TileRef {
@@ -157,7 +158,14 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
                 if (v >= end) break;
                 const bool isx = v < L.vx;
                 const int64_t i = isx ? v : v - L.vx;
-                val[u] = __ldcs(reinterpret_cast<const uint4*>(isx ? L.srcX : L.srcY) + i);
+                if (gp.cast) {   // a1: fp32 -> bf16 round-to-nearest-even (DESIGN R11)
+                    const float4* src = reinterpret_cast<const float4*>(isx ? L.srcX : L.srcY) + 2 * i;
+                    const float4 lo = __ldcs(src), hi = __ldcs(src + 1);
+                    val[u] = make_uint4(pack_bf16x2(lo.x, lo.y), pack_bf16x2(lo.z, lo.w),
+                                        pack_bf16x2(hi.x, hi.y), pack_bf16x2(hi.z, hi.w));
+                } else {
+                    val[u] = __ldcs(reinterpret_cast<const uint4*>(isx ? L.srcX : L.srcY) + i);
+                }
                 off[u] = isx ? L.off_x + (static_cast<size_t>(gp.slot) * L.vx + i) * 16
                              : L.off_dy + (static_cast<size_t>(gp.slot) * L.vy + i) * 16;
             }
@@ -616,6 +624,7 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
         return e ? std::atoi(e) : 0;
     }();
     gp.dbg = dbg;
+    gp.cast = FUSED && fg->cast ? 1 : 0;
     auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED>;
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {

@@ -39,7 +39,7 @@ struct ReconArgs {
     float* V;
     float lr, mu, wd;
     // fused NVLink all-gather (push of this rank's factors inside the reconstruction kernel)
-    const void* srcX;      // X_r, dY_r (wire dtype == in dtype)
+    const void* srcX;      // X_r, dY_r (in dtype: wire dtype, or fp32 with FusedGather::cast)
     const void* srcY;
     void* win;             // ncclWindow_t of the layer's symmetric window
     uint64_t off_x, off_dy, off_flag;
@@ -51,6 +51,7 @@ struct FusedGather {
     int npeers;            // LSA team size (== comm size)
     int me;                // LSA rank (== comm rank)
     void* mc_base;         // NVLS multicast base (multimem.st to every GPU at once), or nullptr
+    bool cast;             // sources are fp32, the wire is bf16 (RNE cast inside the push)
 };
 
 // Tensor-core path (tcgen05 + TMEM + TMA). Requires 16-byte aligned rows (see recon_tc_ok).

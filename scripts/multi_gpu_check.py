@@ -90,6 +90,14 @@ def main():
     record("int_bit_exact", np.array_equal(got.view(np.uint32), want.view(np.uint32))
            and len(set(hashes)) == 1, max_abs=float(np.abs(got - want).max()))
 
+    # 2b: the same through the fp32 -> bf16 cast fused into the push (integers are exact in bf16)
+    dW, dense, hashes, Xall, dYall, Xe, dYe = run(61, 0, 520, 264, 24, "int3", "int3", "f32", "bf16", "f32")
+    S = oracle.sfb_sum(Xall, dYall)
+    want = S.astype(np.float32) * np.float32(1.0 / (n * 24))
+    got = dW.cpu().numpy()
+    record("int_bit_exact_cast", np.array_equal(got.view(np.uint32), want.view(np.uint32))
+           and len(set(hashes)) == 1, max_abs=float(np.abs(got - want).max()))
+
     # 5: fp32 toy (config 1) and fp32 -> bf16 wire with a bf16 dW
     dW, dense, hashes, Xall, dYall, Xe, dYe = run(1, 0, 64, 32, 4, "normal", "normal", "f32", "f32", "f32")
     e = rel_fro(dW.cpu().numpy(), oracle.sfb_dw(Xall, dYall))
