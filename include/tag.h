@@ -181,8 +181,8 @@ tag_status_t tag_sfb_sync_host(tag_sfb_plan_t plan, const void* X_host, const vo
 /* ------------------------------------------------------------------------------------------ */
 /* Buckets: several layers synchronised together                                             */
 /* ------------------------------------------------------------------------------------------ */
-/* A group (bucket) of 1..8 plans of the same comm and the same in/wire/out dtypes, without
- * fuse_sgd. tag_sfb_group_sync runs steps a1-a4 of every layer with ONE push kernel (one LSA
+/* A group (bucket) of 1..8 plans of the same comm, the same in/wire/out dtypes and the same
+ * fuse_sgd setting (and SGD hyper-parameters). tag_sfb_group_sync runs steps a1-a4 of every layer with ONE push kernel (one LSA
  * barrier; or one grouped NCCL call) and ONE persistent tensor-core launch over all layers' output
  * tiles, so launch latency, pipeline ramp-up, the last partial wave and the barrier latency are
  * paid once per bucket instead of once per layer. Results are bitwise identical to calling
@@ -194,6 +194,12 @@ tag_status_t tag_sfb_group_create(const tag_sfb_plan_t* plans, int count, tag_sf
 tag_status_t tag_sfb_group_destroy(tag_sfb_group_t group);
 tag_status_t tag_sfb_group_sync(tag_sfb_group_t group, const void* const* X,
                                 const void* const* dY, void* const* dW, tag_stream_t stream);
+/* Same with the SGD-momentum epilogue of every layer fused (all plans need fuse_sgd = 1 and the
+ * same lr / momentum / weight_decay): W[i], v[i] fp32 M x N in place; dW may be NULL (no dW
+ * written) or an array whose entries may be NULL. */
+tag_status_t tag_sfb_group_sync_sgd(tag_sfb_group_t group, const void* const* X,
+                                    const void* const* dY, float* const* W, float* const* v,
+                                    void* const* dW, tag_stream_t stream);
 /* Stage split, as for single plans: gather = a1 + a2 of every layer, reconstruct = a3 + a4. */
 tag_status_t tag_sfb_group_gather(tag_sfb_group_t group, const void* const* X,
                                   const void* const* dY, tag_stream_t stream);

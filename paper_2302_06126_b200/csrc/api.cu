@@ -275,8 +275,8 @@ bool fusable(const tag_plan_s* p, void* dW) {
 }
 
 tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* X,
-                        const void* const* dY, void* const* dW, bool sgd, float* W, float* V,
-                        cudaStream_t s) {
+                        const void* const* dY, void* const* dW, bool sgd, float* const* W,
+                        float* const* V, cudaStream_t s) {
     tag_comm_s* c = plans[0]->comm;
     ReconArgs a[MAX_GROUP];
     for (int i = 0; i < count; ++i) {
@@ -295,8 +295,8 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
         a[i].out = p->d.out_dtype;
         a[i].alpha = p->alpha;
         a[i].sgd = sgd;
-        a[i].W = W;
-        a[i].V = V;
+        a[i].W = sgd ? W[i] : nullptr;
+        a[i].V = sgd ? V[i] : nullptr;
         a[i].lr = p->d.lr;
         a[i].mu = p->d.momentum;
         a[i].wd = p->d.weight_decay;
@@ -573,7 +573,7 @@ tag_status_t tag_sfb_sync_sgd(tag_sfb_plan_t p, const void* X, const void* dY, f
     TAG_TRY(set_device(p->comm));
     TAG_TRY(check_async(p->comm));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (fusable(p, dW_out)) return fused_sync(&p, 1, &X, &dY, &dW_out, true, W, v, s);
+    if (fusable(p, dW_out)) return fused_sync(&p, 1, &X, &dY, &dW_out, true, &W, &v, s);
     TAG_TRY(do_gather(p, X, dY, s));
     return do_recon(p, dW_out, true, W, v, p->K, p->alpha, s);
 }
@@ -680,8 +680,11 @@ tag_status_t tag_sfb_group_create(const tag_sfb_plan_t* plans, int count, tag_sf
             p->d.wire_dtype != plans[0]->d.wire_dtype || p->d.out_dtype != plans[0]->d.out_dtype)
             return fail(TAG_ERR_INVALID_ARG,
                         "tag_sfb_group_create: plans must share the comm and the dtypes");
-        if (p->d.fuse_sgd)
-            return fail(TAG_ERR_UNSUPPORTED, "tag_sfb_group_create: fuse_sgd plans are not groupable");
+        if (p->d.fuse_sgd != plans[0]->d.fuse_sgd ||
+            (p->d.fuse_sgd && (p->d.lr != plans[0]->d.lr || p->d.momentum != plans[0]->d.momentum ||
+                               p->d.weight_decay != plans[0]->d.weight_decay)))
+            return fail(TAG_ERR_INVALID_ARG,
+                        "tag_sfb_group_create: plans must share fuse_sgd and its hyper-parameters");
         for (int j = 0; j < i; ++j)
             if (plans[j] == p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_create: duplicate plan");
     }
@@ -746,11 +749,12 @@ tag_status_t tag_sfb_group_gather(tag_sfb_group_t g, const void* const* X, const
     return st;
 }
 
-tag_status_t tag_sfb_group_reconstruct(tag_sfb_group_t g, void* const* dW, tag_stream_t stream) {
-    if (!g || !dW) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_reconstruct: NULL argument");
+static tag_status_t group_reconstruct(tag_sfb_group_t g, void* const* dW, bool sgd,
+                                      float* const* W, float* const* V, tag_stream_t stream) {
     const int count = static_cast<int>(g->plans.size());
     for (int i = 0; i < count; ++i) {
-        TAG_TRY(check_ptrs("tag_sfb_group_reconstruct", {dW[i]}));
+        if (!sgd || dW[i]) TAG_TRY(check_ptrs("tag_sfb_group_reconstruct", {dW[i]}));
+        if (sgd) TAG_TRY(check_ptrs("tag_sfb_group_sync_sgd", {W[i], V[i]}));
         if (!g->plans[i]->src_x)
             return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_reconstruct: no factors gathered yet");
     }
@@ -770,18 +774,58 @@ tag_status_t tag_sfb_group_reconstruct(tag_sfb_group_t g, void* const* dW, tag_s
         a[i].wire = p->d.wire_dtype;
         a[i].out = p->d.out_dtype;
         a[i].alpha = p->alpha;
+        a[i].sgd = sgd;
+        a[i].W = sgd ? W[i] : nullptr;
+        a[i].V = sgd ? V[i] : nullptr;
+        a[i].lr = p->d.lr;
+        a[i].mu = p->d.momentum;
+        a[i].wd = p->d.weight_decay;
         tc = tc && recon_tc_ok(a[i]);
     }
     if (tc) return launch_recon_tc_group(a, count, s);
     for (int i = 0; i < count; ++i)
-        TAG_TRY(do_recon(g->plans[i], dW[i], false, nullptr, nullptr, g->plans[i]->K,
-                         g->plans[i]->alpha, s));
+        TAG_TRY(do_recon(g->plans[i], dW[i], sgd, sgd ? W[i] : nullptr, sgd ? V[i] : nullptr,
+                         g->plans[i]->K, g->plans[i]->alpha, s));
     return TAG_OK;
+}
+
+tag_status_t tag_sfb_group_reconstruct(tag_sfb_group_t g, void* const* dW, tag_stream_t stream) {
+    if (!g || !dW) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_reconstruct: NULL argument");
+    if (g->plans[0]->d.fuse_sgd)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_reconstruct: fuse_sgd group, use sync_sgd");
+    return group_reconstruct(g, dW, false, nullptr, nullptr, stream);
+}
+
+tag_status_t tag_sfb_group_sync_sgd(tag_sfb_group_t g, const void* const* X, const void* const* dY,
+                                    float* const* W, float* const* v, void* const* dW,
+                                    tag_stream_t stream) {
+    if (!g || !X || !dY || !W || !v)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync_sgd: NULL argument");
+    if (!g->plans[0]->d.fuse_sgd)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync_sgd: plans have fuse_sgd = 0");
+    const int count = static_cast<int>(g->plans.size());
+    void* none[MAX_GROUP] = {nullptr};
+    void* const* dWs = dW ? dW : none;
+    bool fuse = true;
+    for (int i = 0; i < count; ++i) {
+        TAG_TRY(check_ptrs("tag_sfb_group_sync_sgd", {X[i], dY[i], W[i], v[i]}));
+        if (dWs[i]) TAG_TRY(check_ptrs("tag_sfb_group_sync_sgd", {dWs[i]}));
+        fuse = fuse && fusable(g->plans[i], dWs[i]);
+    }
+    TAG_TRY(set_device(g->plans[0]->comm));
+    TAG_TRY(check_async(g->plans[0]->comm));
+    if (fuse)
+        return fused_sync(g->plans.data(), count, X, dY, dWs, true, W, v,
+                          reinterpret_cast<cudaStream_t>(stream));
+    TAG_TRY(tag_sfb_group_gather(g, X, dY, stream));
+    return group_reconstruct(g, dWs, true, W, v, stream);
 }
 
 tag_status_t tag_sfb_group_sync(tag_sfb_group_t g, const void* const* X, const void* const* dY,
                                 void* const* dW, tag_stream_t stream) {
     if (!g || !X || !dY || !dW) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync: NULL argument");
+    if (g->plans[0]->d.fuse_sgd)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync: fuse_sgd group, use sync_sgd");
     const int count = static_cast<int>(g->plans.size());
     bool fuse = true;
     for (int i = 0; i < count; ++i) {

@@ -82,6 +82,7 @@ _SIGS = {
     "tag_sfb_group_destroy": ([_vp], _st),
     "tag_sfb_group_sync": ([_vp, _p(_vp), _p(_vp), _p(_vp), _vp], _st),
     "tag_sfb_group_gather": ([_vp, _p(_vp), _p(_vp), _vp], _st),
+    "tag_sfb_group_sync_sgd": ([_vp, _p(_vp), _p(_vp), _p(_vp), _p(_vp), _p(_vp), _vp], _st),
     "tag_sfb_group_reconstruct": ([_vp, _p(_vp), _vp], _st),
 }
 for _name, (_args, _res) in _SIGS.items():
@@ -287,6 +288,14 @@ class SfbGroup:
     def sync(self, Xs, dYs, dWs, stream=None):
         _check(_lib.tag_sfb_group_sync(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"),
                                        self._ptrs(dWs, "dW"), _stream(stream)), "tag_sfb_group_sync")
+
+    def sync_sgd(self, Xs, dYs, Ws, vs, dWs=None, stream=None):
+        shapes = [(p.M, p.N) for p in self.plans]
+        W = (_vp * len(self.plans))(*[_dev(w, torch.float32, s, "W") for w, s in zip(Ws, shapes)])
+        v = (_vp * len(self.plans))(*[_dev(x, torch.float32, s, "v") for x, s in zip(vs, shapes)])
+        dW = self._ptrs(dWs, "dW") if dWs is not None else None
+        _check(_lib.tag_sfb_group_sync_sgd(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"), W,
+                                           v, dW, _stream(stream)), "tag_sfb_group_sync_sgd")
 
     def gather(self, Xs, dYs, stream=None):
         _check(_lib.tag_sfb_group_gather(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"),

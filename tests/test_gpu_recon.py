@@ -307,3 +307,37 @@ def test_group_validation(tag, comm1):
         tag.SfbGroup([])
     a.close()
     b.close()
+
+
+def test_group_sgd_equals_per_plan(tag, comm1):
+    """BERT-large bucket (FFN1, FFN2, pooler; virtual n = 8) with the SGD epilogue fused: one
+    grouped launch == tag_sfb_sync_sgd per layer, bit for bit (W, v and dW)."""
+    hp = dict(lr=1e-3, momentum=0.9, weight_decay=1e-4)
+    specs = [(1024, 4096, 8 * 128, "normal"), (4096, 1024, 8 * 128, "gelu"), (1024, 1024, 8 * 2, "tanh")]
+    plans, Xs, dYs, W1, v1, W2, v2, d1, d2 = [], [], [], [], [], [], [], [], []
+    for li, (M, N, K, xd) in enumerate(specs):
+        X = synth.draw(xd, K, M, synth.rng(80, li, 0, 0))
+        dY = synth.draw("small", K, N, synth.rng(80, li, 0, 1))
+        W0, _ = synth.sgd_state(80, li, M, N)
+        p = tag.SfbPlan(comm1, M, N, K, "bf16", "bf16", "f32", fuse_sgd=True, **hp)
+        plans.append(p)
+        Xs.append(to_dev(X, "bf16"))
+        dYs.append(to_dev(dY, "bf16"))
+        for Wl, vl, dl in ((W1, v1, d1), (W2, v2, d2)):
+            Wl.append(torch.from_numpy(W0).cuda())
+            vl.append(torch.zeros(M, N, device="cuda"))
+            dl.append(torch.empty(M, N, device="cuda"))
+    for _ in range(2):
+        for i, p in enumerate(plans):
+            p.sync_sgd(Xs[i], dYs[i], W1[i], v1[i], d1[i])
+    g = tag.SfbGroup(plans)
+    for _ in range(2):
+        g.sync_sgd(Xs, dYs, W2, v2, d2)
+    torch.cuda.synchronize()
+    for i in range(len(plans)):
+        assert torch.equal(W1[i], W2[i]) and torch.equal(v1[i], v2[i]) and torch.equal(d1[i], d2[i])
+    with pytest.raises(tag.TagError):
+        g.sync(Xs, dYs, d2)                        # fuse_sgd groups only take sync_sgd
+    g.close()
+    for p in plans:
+        p.close()
