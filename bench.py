@@ -227,11 +227,17 @@ def main():
     layers = []
     for li, L in enumerate(cfg.layers):
         X, dY = synth.factors(cfg.cid, li, rank, L.M, L.N, L.B, L.x_dist, L.dy_dist)
-        plan = tag.SfbPlan(comm, L.M, L.N, L.B, cfg.in_dtype, cfg.wire_dtype, cfg.out_dtype)
+        sgd = cfg.sgd or {}
+        plan = tag.SfbPlan(comm, L.M, L.N, L.B, cfg.in_dtype, cfg.wire_dtype, cfg.out_dtype,
+                           fuse_sgd=bool(sgd), **sgd)
         Xh = torch.from_numpy(X).to(tdt[cfg.in_dtype]).pin_memory()
         dYh = torch.from_numpy(dY).to(tdt[cfg.in_dtype]).pin_memory()
-        layers.append(dict(L=L, plan=plan, X=Xh.cuda(), dY=dYh.cuda(), Xh=Xh, dYh=dYh,
-                           dW=torch.empty(L.M, L.N, dtype=tdt[cfg.out_dtype], device="cuda")))
+        ent = dict(L=L, plan=plan, X=Xh.cuda(), dY=dYh.cuda(), Xh=Xh, dYh=dYh,
+                   dW=torch.empty(L.M, L.N, dtype=tdt[cfg.out_dtype], device="cuda"))
+        if sgd:   # E2: fp32 master weights and momentum, updated in the epilogue (no dW write)
+            W0, v0 = synth.sgd_state(cfg.cid, li, L.M, L.N)
+            ent["W"], ent["v"] = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
+        layers.append(ent)
     peaks, peak_src = load_peaks()
     choices = tag.select([dict(M=l["L"].M, N=l["L"].N, B=l["L"].B, factor_dtype=cfg.wire_dtype,
                                grad_dtype=cfg.out_dtype) for l in layers], n,
@@ -253,13 +259,20 @@ def main():
 
     def step():
         with torch.cuda.stream(stream):
-            if group is not None:
+            if group is not None and cfg.sgd:
+                # E2: the optimizer step is fused into the same single launch, dW never stored
+                group.sync_sgd(Xs, dYs, [l["W"] for l in layers], [l["v"] for l in layers], None,
+                               stream)
+            elif group is not None:
                 # one call: at n > 1 a single fused kernel pushes the factors over NVLink and
                 # reconstructs every layer (tag_sfb_group_sync); at n = 1 the reconstruction only
                 group.sync(Xs, dYs, dWs, stream)
             else:
                 for l in layers:
-                    l["plan"].sync(l["X"], l["dY"], l["dW"], stream)
+                    if cfg.sgd:
+                        l["plan"].sync_sgd(l["X"], l["dY"], l["W"], l["v"], None, stream)
+                    else:
+                        l["plan"].sync(l["X"], l["dY"], l["dW"], stream)
 
     def start_events(k):
         flush_l2()
@@ -310,9 +323,13 @@ def main():
             evs = start_events(2 * nl + 1)
             with torch.cuda.stream(stream):
                 for i, l in enumerate(layers):
-                    l["plan"].gather(l["X"], l["dY"], stream)
-                    evs[2 * i + 1].record(stream)
-                    l["plan"].reconstruct(l["dW"], stream)
+                    if cfg.sgd:           # no stage split with the fused optimizer: whole sync
+                        evs[2 * i + 1].record(stream)
+                        l["plan"].sync_sgd(l["X"], l["dY"], l["W"], l["v"], None, stream)
+                    else:
+                        l["plan"].gather(l["X"], l["dY"], stream)
+                        evs[2 * i + 1].record(stream)
+                        l["plan"].reconstruct(l["dW"], stream)
                     evs[2 * i + 2].record(stream)
             torch.cuda.synchronize()
             for i in range(nl):
@@ -333,7 +350,8 @@ def main():
     tdist.barrier()
     nstaged = max(5, min(args.steps, 30))
     layer_recon_ms, layer_sync_ms = timed_layers(nstaged)
-    staged_g_ms, staged_r_ms = timed_staged(nstaged) if group is not None else ([], [])
+    staged_g_ms, staged_r_ms = (timed_staged(nstaged) if group is not None and not cfg.sgd
+                                else ([], []))
 
     t_step_ms = tdist.max_over_ranks(statistics.mean(steps_ms))
     dw_bytes = sum(l["L"].M * l["L"].N * ESIZE[cfg.out_dtype] for l in layers)
@@ -341,12 +359,15 @@ def main():
 
     # roofline of the dominant kernel. Bucket mode: the step is ONE launch of recon_tc_kernel
     # (with the NVLink push fused in at n > 1), so its duration is the step's.
+    # E2 reads and writes W and v (16 B per element) and stores no dW
     alg_bytes = sum(n * l["L"].B * (l["L"].M + l["L"].N) * ESIZE[cfg.wire_dtype]
-                    + l["L"].M * l["L"].N * ESIZE[cfg.out_dtype] for l in layers)
+                    + l["L"].M * l["L"].N * (16 if cfg.sgd else ESIZE[cfg.out_dtype])
+                    for l in layers)
     if group is not None:
         kernel_ms = t_step_ms
         launches_per_step = 1
-        recon_only_ms = tdist.max_over_ranks(statistics.mean(staged_r_ms))
+        recon_only_ms = (tdist.max_over_ranks(statistics.mean(staged_r_ms)) if staged_r_ms
+                         else kernel_ms)
     else:
         kernel_ms = tdist.max_over_ranks(sum(statistics.mean(r) for r in layer_recon_ms))
         launches_per_step = nl
