@@ -78,6 +78,8 @@ struct LayerParams {
     int M, N;
     int num_n_blocks, num_k_blocks;
     int tile_begin;   // first global tile index of this layer
+    int num_m_blocks;
+    int m_fast;       // 1: consecutive tiles walk down M (share a B panel), else along N
     float alpha;
     // fused all-gather (FUSED = true): this rank's factors are pushed into every peer's window
     const void* srcX;      // X_r (B x M, wire dtype)
@@ -109,6 +111,10 @@ __device__ __forceinline__ TileRef locate(const GroupParams& gp, int tile) {
     int li = 0;
     while (li + 1 < gp.count && tile >= gp.L[li + 1].tile_begin) ++li;
     const int t = tile - gp.L[li].tile_begin;
+    if (gp.L[li].m_fast) {
+        const int nmb = gp.L[li].num_m_blocks;
+        return TileRef{li, (t % nmb) * BM * CTAS, (t / nmb) * BN};
+    }
     const int nnb = gp.L[li].num_n_blocks;
     return TileRef{li, (t / nnb) * BM * CTAS, (t % nnb) * BN};
 }
@@ -579,6 +585,15 @@ int use_ctas(const ReconArgs* a, int count) {
     return 2;
 }
 
+// Big (256 x 256 pair) tiles only when they fill every TPC at least once; a small-output bucket
+// (e.g. Transformer FFN at K = 256: 16 pair tiles) runs faster on 4x as many 128 x 128 tiles.
+bool big_tiles(const ReconArgs* a, int count) {
+    if (!use_wide(a, count)) return false;
+    if (std::getenv("TAG_RECON_BN")) return true;     // experiments force the wide config
+    const int ctas = use_ctas(a, count);
+    return tiles_for(a, count, 256, ctas) >= num_sms() / ctas;
+}
+
 template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED>
 tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
     using C = Cfg<BN, CTAS>;
@@ -599,7 +614,12 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
         L.num_k_blocks = static_cast<int>((a[i].K + BK - 1) / BK);
         L.tile_begin = tiles;
         L.alpha = a[i].alpha;
-        tiles += static_cast<int>((a[i].M + BM * CTAS - 1) / (BM * CTAS)) * L.num_n_blocks;
+        L.num_m_blocks = static_cast<int>((a[i].M + BM * CTAS - 1) / (BM * CTAS));
+        // Raster: when dY_all (K x N) no longer fits comfortably in L2, walk M first so the
+        // concurrently running tiles share each B panel (read once from HBM); otherwise walk N
+        // (whole output rows written together, better DRAM page locality for the epilogue).
+        L.m_fast = (a[i].K * a[i].N * 2 > (32ll << 20)) ? 1 : 0;
+        tiles += L.num_m_blocks * L.num_n_blocks;
         if constexpr (FUSED) {
             L.srcX = a[i].srcX;
             L.srcY = a[i].srcY;
@@ -657,8 +677,8 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
 
 template <bool FUSED>
 tag_status_t dispatch(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
-    const bool wide = use_wide(a, count);
-    const bool pair = use_ctas(a, count) == 2;
+    const bool wide = big_tiles(a, count);
+    const bool pair = wide && use_ctas(a, count) == 2;
     if (a[0].sgd) {
         if (!wide) return launch_t<128, 1, false, true, FUSED>(a, count, s, fg);
         return pair ? launch_t<256, 2, false, true, FUSED>(a, count, s, fg)
@@ -690,8 +710,9 @@ bool recon_tc_ok(const ReconArgs& a) {
 }
 
 int recon_tc_grid(const ReconArgs* a, int count) {
-    const int ctas = use_ctas(a, count);
-    const int tiles = tiles_for(a, count, use_wide(a, count) ? 256 : 128, ctas);
+    const bool wide = big_tiles(a, count);
+    const int ctas = wide ? use_ctas(a, count) : 1;
+    const int tiles = tiles_for(a, count, wide ? 256 : 128, ctas);
     const int units = num_sms() / ctas;
     return ctas * (tiles < units ? tiles : units);
 }
