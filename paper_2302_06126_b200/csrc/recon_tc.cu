@@ -571,10 +571,10 @@ bool use_wide(const ReconArgs* a, int count) {
     int64_t kmax = 0;
     for (int i = 0; i < count; ++i) kmax = a[i].K > kmax ? a[i].K : kmax;
     // Small K (the HBM-write-bound regime of the paper's small-batch layers): BN = 128 tiles,
-    // 4 TMEM accumulators, finer tail. K >= 192: BN = 256 on a CTA pair (cta_group::2, 256 x 256
-    // tiles): the operand re-reads from L2 bind first there (fc6 at K = 256, one CTA: 102 us at
-    // BN = 128, 88 us at BN = 256 with L2 throughput saturated), and the pair halves them again.
-    bool wide = kmax >= 192;
+    // 4 TMEM accumulators, finer tail. K >= 96: BN = 256 (and a CTA pair, cta_group::2, from
+    // K = 192): the operand re-reads from L2 bind first there (fc6 at K = 256, one CTA: 102 us
+    // at BN = 128, 88 us at BN = 256 with L2 throughput saturated); the pair halves B's again.
+    bool wide = kmax >= 96;
     if (const char* e = std::getenv("TAG_RECON_BN")) wide = std::atoi(e) == 256;   // experiments
     return wide;
 }
@@ -582,7 +582,11 @@ bool use_wide(const ReconArgs* a, int count) {
 int use_ctas(const ReconArgs* a, int count) {
     if (!use_wide(a, count)) return 1;
     if (const char* e = std::getenv("TAG_RECON_CTAS")) return std::atoi(e) == 1 ? 1 : 2;
-    return 2;
+    int64_t kmax = 0;
+    for (int i = 0; i < count; ++i) kmax = a[i].K > kmax ? a[i].K : kmax;
+    // measured on the VGG-19 bucket (scripts/tile_sweep.py): K = 128 one CTA x 256 columns 96 us
+    // (pairs 101, 128-col tiles 99); K = 256 pairs 107 us (one CTA 112)
+    return kmax >= 192 ? 2 : 1;
 }
 
 // Big (256 x 256 pair) tiles only when they fill every TPC at least once; a small-output bucket
