@@ -66,7 +66,7 @@ def expected_int(oracle_mod, Xall, dYall, n_times_b, out_dt):
 # tensor-core shapes (M, N multiples of 8) and SIMT shapes (odd), K = n*B with ragged tails
 TC_SHAPES = [(64, 32, 8), (128, 256, 32), (136, 264, 40), (520, 1000, 64), (1024, 4096, 256),
              (256, 512, 5), (8, 8, 1), (384, 768, 2048), (4096, 1000, 256), (200, 264, 300),
-             (128, 8, 33), (8, 136, 512)]
+             (128, 8, 33), (8, 136, 512), (264, 520, 100), (4096, 1024, 128)]
 SIMT_SHAPES = [(1, 1, 2), (3, 5, 6), (17, 33, 12), (130, 257, 10)]
 
 
