@@ -486,11 +486,29 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                     const bool col_ok = gcol < N;   // N % 8 == 0: a 16-B slot is all in or out
                     const int64_t off0 = static_cast<int64_t>(row0 + sub) * N + gcol;
                     const int64_t step = 4 * static_cast<int64_t>(N);
+                    // warp-uniform: every row and column of this 32 x 128-B chunk is in range
+                    const bool full = row0 + 32 <= M &&
+                                      n0 + half * (BN / 2) + (ch + q + 1) * COLS_PER_CHUNK <= N;
+                    const uint32_t sq = sbuf + q * 4096 + sub * 128;
+                    const uint32_t sw0 = (cj ^ sub) << 4, sw1 = (cj ^ (sub + 4)) << 4;
+                    if (full && !SGD) {
+                        // fast path (all but the edge tiles): no per-store predicates, the global
+                        // address advances by 4 rows per store
+                        uint4* gp4 = reinterpret_cast<uint4*>(Cp + off0 * ESZ);
+                        const int64_t gstep = step * ESZ / 16;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            uint32_t a, b, c, d;
+                            ptx::ld_shared_v4(sq + i * 512 + ((i & 1) ? sw1 : sw0), a, b, c, d);
+                            __stcs(gp4 + i * gstep, make_uint4(a, b, c, d));
+                        }
+                        continue;
+                    }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int r = 4 * i + sub;
                         uint32_t a, b, c, d;
-                        ptx::ld_shared_v4(sbuf + q * 4096 + r * 128 + ((cj ^ (r & 7)) << 4), a, b, c, d);
+                        ptx::ld_shared_v4(sq + i * 512 + ((i & 1) ? sw1 : sw0), a, b, c, d);
                         if (!col_ok || row0 + r >= M) continue;
                         const int64_t off = off0 + i * step;
                         if constexpr (SGD) {
