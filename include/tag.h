@@ -178,6 +178,20 @@ tag_status_t tag_sfb_sync_sgd(tag_sfb_plan_t plan, const void* X, const void* dY
 tag_status_t tag_sfb_sync_host(tag_sfb_plan_t plan, const void* X_host, const void* dY_host,
                                void* dW_host, tag_stream_t stream);
 
+/* Sharded reconstruction: rank r reconstructs only rows
+ * [row_begin, row_begin + row_count) of dW — a contiguous run of 128-row tiles — so each GPU
+ * writes M*N/n gradient elements instead of M*N (the HBM write is the reconstruction's binding
+ * roof). Every rank still receives all factors; the shards of ranks 0..n-1 tile dW exactly, in
+ * rank order, and each shard is bitwise equal to the same rows of tag_sfb_sync's dW. This is a
+ * variant, not the paper's semantics (the paper's Duplicate leaves the full gradient on every
+ * replica): it fits a sharded (ZeRO-style) optimizer. tag_sfb_shard_rows is a host
+ * query; row_count may be 0 (more ranks than 128-row tiles). */
+tag_status_t tag_sfb_shard_rows(tag_sfb_plan_t plan, int rank, int64_t* row_begin,
+                                int64_t* row_count);
+/* COLLECTIVE (n > 1). dW_shard: row_count x N in out_dtype (may be NULL when row_count == 0). */
+tag_status_t tag_sfb_sync_sharded(tag_sfb_plan_t plan, const void* X, const void* dY,
+                                  void* dW_shard, tag_stream_t stream);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Buckets: several layers synchronised together                                             */
 /* ------------------------------------------------------------------------------------------ */

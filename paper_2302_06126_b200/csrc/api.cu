@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -274,9 +275,19 @@ bool fusable(const tag_plan_s* p, void* dW) {
     return recon_tc_ok(a);
 }
 
+void shard_range(const tag_plan_s* p, int rank, int64_t* begin, int64_t* cnt) {
+    const int64_t n = p->d.n, M = p->d.M;
+    const int64_t tiles = (M + 127) / 128;
+    const int64_t per = (tiles + n - 1) / n;                 // 128-row tiles per rank
+    const int64_t b = std::min(M, rank * per * 128);
+    const int64_t e = std::min(M, (rank + 1) * per * 128);
+    *begin = b;
+    *cnt = e - b;
+}
+
 tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* X,
                         const void* const* dY, void* const* dW, bool sgd, float* const* W,
-                        float* const* V, cudaStream_t s) {
+                        float* const* V, cudaStream_t s, bool sharded = false) {
     tag_comm_s* c = plans[0]->comm;
     ReconArgs a[MAX_GROUP];
     for (int i = 0; i < count; ++i) {
@@ -308,6 +319,13 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
         a[i].off_flag = p->win_flag_off + 4 * static_cast<size_t>(p->parity);
         a[i].cx = p->d.B * p->d.M;
         a[i].cy = p->d.B * p->d.N;
+        if (sharded) {
+            int64_t rb, rc;
+            shard_range(p, c->rank, &rb, &rc);
+            a[i].A = static_cast<const char*>(a[i].A) + rb * ew;   // columns rb.. of X_all
+            a[i].lda = p->d.M;
+            a[i].M = rc;
+        }
     }
     // every CTA of every rank adds 1 per layer: the counter grows by n * grid per call
     const uint32_t inc = static_cast<uint32_t>(c->nranks) * static_cast<uint32_t>(recon_tc_grid(a, count));
@@ -318,7 +336,7 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
     for (int i = 0; i < count; ++i) {
         tag_plan_s* p = plans[i];
         p->flag_total[p->parity] += inc;
-        p->src_x = a[i].A;
+        p->src_x = static_cast<char*>(p->win_base) + a[i].off_x;     // the full X_all
         p->src_dy = a[i].Bm;
         p->parity ^= 1;
     }
@@ -576,6 +594,47 @@ tag_status_t tag_sfb_sync_sgd(tag_sfb_plan_t p, const void* X, const void* dY, f
     if (fusable(p, dW_out)) return fused_sync(&p, 1, &X, &dY, &dW_out, true, &W, &v, s);
     TAG_TRY(do_gather(p, X, dY, s));
     return do_recon(p, dW_out, true, W, v, p->K, p->alpha, s);
+}
+
+tag_status_t tag_sfb_shard_rows(tag_sfb_plan_t p, int rank, int64_t* row_begin, int64_t* row_count) {
+    if (!p || !row_begin || !row_count) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_shard_rows: NULL argument");
+    if (rank < 0 || rank >= p->d.n) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_shard_rows: bad rank");
+    shard_range(p, rank, row_begin, row_count);
+    return TAG_OK;
+}
+
+tag_status_t tag_sfb_sync_sharded(tag_sfb_plan_t p, const void* X, const void* dY, void* dW_shard,
+                                  tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded: NULL plan");
+    int64_t rb, rc;
+    shard_range(p, p->comm->rank, &rb, &rc);
+    TAG_TRY(check_ptrs("tag_sfb_sync_sharded", {X, dY}));
+    if (rc > 0) TAG_TRY(check_ptrs("tag_sfb_sync_sharded", {dW_shard}));
+    TAG_TRY(set_device(p->comm));
+    TAG_TRY(check_async(p->comm));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    // the fused kernel needs at least one tile on every rank (its CTAs push the factors)
+    if (rc > 0 && fusable(p, dW_shard))
+        return fused_sync(&p, 1, &X, &dY, &dW_shard, false, nullptr, nullptr, s, true);
+    TAG_TRY(do_gather(p, X, dY, s));
+    if (rc == 0) return TAG_OK;
+    const size_t ew = dtype_size(p->d.wire_dtype);
+    const void* full_x = p->src_x;
+    p->src_x = static_cast<const char*>(full_x) + rb * ew;
+    ReconArgs a{};
+    a.A = p->src_x;
+    a.Bm = p->src_dy;
+    a.C = dW_shard;
+    a.M = rc;
+    a.N = p->d.N;
+    a.K = p->K;
+    a.lda = p->d.M;
+    a.wire = p->d.wire_dtype;
+    a.out = p->d.out_dtype;
+    a.alpha = p->alpha;
+    tag_status_t st = (p->use_tc && recon_tc_ok(a)) ? launch_recon_tc(a, s) : launch_recon_simt(a, s);
+    p->src_x = full_x;
+    return st;
 }
 
 tag_status_t tag_sfb_sync_host(tag_sfb_plan_t p, const void* X_host, const void* dY_host,

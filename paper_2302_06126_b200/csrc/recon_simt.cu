@@ -24,7 +24,7 @@ __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return _
 template <typename T, bool OUT_BF16, bool SGD>
 __global__ void __launch_bounds__(256)
 recon_simt_kernel(const T* __restrict__ A, const T* __restrict__ Bm, void* __restrict__ C,
-                  int M, int N, int K, float alpha, float* __restrict__ W,
+                  int M, int N, int K, int64_t lda, float alpha, float* __restrict__ W,
                   float* __restrict__ V, float lr, float mu, float wd)
 {
     __shared__ float As[TK][TM];
@@ -36,7 +36,7 @@ recon_simt_kernel(const T* __restrict__ A, const T* __restrict__ Bm, void* __res
         for (int i = threadIdx.x; i < TK * TM; i += 256) {
             const int kk = i / TM, mm = i % TM;
             const int k = k0 + kk, m = m0 + mm;
-            As[kk][mm] = (k < K && m < M) ? to_f(A[static_cast<int64_t>(k) * M + m]) : 0.f;
+            As[kk][mm] = (k < K && m < M) ? to_f(A[static_cast<int64_t>(k) * lda + m]) : 0.f;
         }
         for (int i = threadIdx.x; i < TK * TN; i += 256) {
             const int kk = i / TN, nn = i % TN;
@@ -85,7 +85,8 @@ tag_status_t launch_t(const ReconArgs& a, cudaStream_t s) {
     if (grid.y > 65535) return fail(TAG_ERR_UNSUPPORTED, "recon_simt: M too large");
     recon_simt_kernel<T, OUT_BF16, SGD><<<grid, 256, 0, s>>>(
         static_cast<const T*>(a.A), static_cast<const T*>(a.Bm), a.C, static_cast<int>(a.M),
-        static_cast<int>(a.N), static_cast<int>(a.K), a.alpha, a.W, a.V, a.lr, a.mu, a.wd);
+        static_cast<int>(a.N), static_cast<int>(a.K), a.lda ? a.lda : a.M, a.alpha, a.W, a.V, a.lr,
+        a.mu, a.wd);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "launch recon_simt_kernel");
     count_launch();

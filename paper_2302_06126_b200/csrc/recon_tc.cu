@@ -565,11 +565,11 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // Row-major rows x cols matrix; box = box_cols x box_rows; 128-byte swizzle.
 bool encode_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esize, int64_t rows,
-               int64_t cols, int box_cols, int box_rows) {
+               int64_t cols, int box_cols, int box_rows, int64_t ld = 0) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols * esize)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>((ld ? ld : cols) * esize)};
     cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
@@ -624,7 +624,8 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     int tiles = 0;
     for (int i = 0; i < count; ++i) {
         LayerParams& L = gp.L[i];
-        if (!encode_2d(&L.tmA, a[i].A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a[i].K, a[i].M, 64, BK) ||
+        if (!encode_2d(&L.tmA, a[i].A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a[i].K, a[i].M, 64, BK,
+                       a[i].lda) ||
             !encode_2d(&L.tmB, a[i].Bm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a[i].K, a[i].N, 64, BK))
             return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
         L.C = a[i].C;
@@ -720,7 +721,7 @@ tag_status_t dispatch(const ReconArgs* a, int count, cudaStream_t s, const Fused
 
 bool recon_tc_ok(const ReconArgs& a) {
     if (a.wire != TAG_BF16) return false;                 // tf32 path: later
-    if (a.M % 8 || a.N % 8) return false;                 // 16-byte rows for TMA (bf16)
+    if (a.M % 8 || a.N % 8 || a.lda % 8) return false;   // 16-byte rows for TMA (bf16)
     if (a.M > INT32_MAX || a.N > INT32_MAX || a.K > INT32_MAX) return false;
     if (a.sgd && a.out == TAG_BF16 && a.C) return false;  // E2 writes fp32 dW only
     if (reinterpret_cast<uintptr_t>(a.A) % 16 || reinterpret_cast<uintptr_t>(a.Bm) % 16)

@@ -30,6 +30,7 @@ struct ReconArgs {
     const void* Bm;      // K x N
     void* C;             // M x N, out dtype; may be nullptr when sgd (no dW write)
     int64_t M, N, K;
+    int64_t lda;         // elements between consecutive rows of A (0: M) — row shards of X_all
     tag_dtype_t wire;    // operand dtype
     tag_dtype_t out;     // C dtype
     float alpha;

@@ -74,6 +74,8 @@ _SIGS = {
     "tag_sfb_reconstruct": ([_vp, _vp, _vp], _st),
     "tag_sfb_sync_sgd": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_sync_host": ([_vp, _vp, _vp, _vp, _vp], _st),
+    "tag_sfb_shard_rows": ([_vp, _i, _p(ctypes.c_int64), _p(ctypes.c_int64)], _st),
+    "tag_sfb_sync_sharded": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_local_grad": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_dense_allreduce": ([_vp, _vp, _vp], _st),
     "tag_sgd_step": ([_vp, _vp, _vp, _vp, _vp], _st),
@@ -229,6 +231,21 @@ class SfbPlan:
         _check(_lib.tag_sfb_sync_sgd(self._h, x, dy, _dev(W, torch.float32, shape, "W"),
                                      _dev(v, torch.float32, shape, "v"), dw, _stream(stream)),
                "tag_sfb_sync_sgd")
+
+    def shard_rows(self, rank=None):
+        """(row_begin, row_count) of `rank`'s dW shard (default: this rank)."""
+        b, c = ctypes.c_int64(), ctypes.c_int64()
+        _check(_lib.tag_sfb_shard_rows(self._h, self.comm.rank if rank is None else rank,
+                                       ctypes.byref(b), ctypes.byref(c)), "tag_sfb_shard_rows")
+        return b.value, c.value
+
+    def sync_sharded(self, X, dY, dW_shard, stream=None):
+        x, dy = self._xy(X, dY)
+        _, rc = self.shard_rows()
+        dw = _dev(dW_shard, self.out_torch, (rc, self.N), "dW_shard") if rc > 0 else _vp()
+        _check(_lib.tag_sfb_sync_sharded(self._h, x, dy, dw, _stream(stream)),
+               "tag_sfb_sync_sharded")
+        return dW_shard
 
     def sync_host(self, X_host, dY_host, dW_host, stream=None):
         _check(_lib.tag_sfb_sync_host(

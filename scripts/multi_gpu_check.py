@@ -148,6 +148,28 @@ def main():
     for p in plans:
         p.close()
 
+    # 9: sharded reconstruction: each rank's rows == the same rows of the full dW, bit for bit,
+    #    and the shards tile dW (fc6-sized factors, fused path; and an odd shape via the SIMT path)
+    for li, (M, N, B, xd, dyd, out_dt) in enumerate([(25088, 4096, 32, "relu", "masked_small", "f32"),
+                                                     (1000, 264, 16, "int3", "int3", "bf16"),
+                                                     (130, 257, 5, "int3", "int3", "f32")]):
+        X, dY = synth.factors(3, 20 + li, rank, M, N, B, xd, dyd)
+        plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", out_dt)
+        Xd = torch.from_numpy(X).to(torch.bfloat16).cuda()
+        dYd = torch.from_numpy(dY).to(torch.bfloat16).cuda()
+        full = torch.empty(M, N, dtype=TDT[out_dt], device="cuda")
+        plan.sync(Xd, dYd, full)
+        rb, rc = plan.shard_rows()
+        shard = torch.full((max(rc, 1), N), float("nan"), dtype=TDT[out_dt], device="cuda")[:rc]
+        for _ in range(2):
+            plan.sync_sharded(Xd, dYd, shard)
+        torch.cuda.synchronize()
+        ranges = tdist.all_gather_object((rb, rc))
+        tiles_ok = ranges[0][0] == 0 and sum(c for _, c in ranges) == M and all(
+            ranges[i][0] + ranges[i][1] == ranges[i + 1][0] for i in range(n - 1))
+        record(f"sharded_{M}x{N}", torch.equal(shard, full[rb:rb + rc]) and tiles_ok, rows=[rb, rc])
+        plan.close()
+
     # 7: selector identical on all ranks and equal to the oracle
     lays = [dict(M=L.M, N=L.N, B=L.B) for c in (2, 3, 4, 5) for L in synth.CONFIGS[c].layers]
     got = tag.select([dict(l, factor_dtype="bf16", grad_dtype="f32") for l in lays], n,
