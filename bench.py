@@ -446,8 +446,11 @@ def main():
                                       device="cuda")[:rc])
         def sharded_step():
             with torch.cuda.stream(stream):
-                for l, sh in zip(layers, shards):
-                    l["plan"].sync_sharded(l["X"], l["dY"], sh, stream)
+                if group is not None:        # one fused launch for the bucket's shards
+                    group.sync_sharded(Xs, dYs, shards, stream)
+                else:
+                    for l, sh in zip(layers, shards):
+                        l["plan"].sync_sharded(l["X"], l["dY"], sh, stream)
         for _ in range(3):
             sharded_step()
         ts = []
@@ -460,7 +463,7 @@ def main():
         t_sh = tdist.max_over_ranks(statistics.mean(ts))
         sharded = {"ms_per_step": round(t_sh, 4),
                    "dW_GBps_all_ranks": round(dw_bytes / (t_sh * 1e-3) / 1e9, 1),
-                   "note": "each rank reconstructs M/n rows of every layer (tag_sfb_sync_sharded)"}
+                   "note": "each rank reconstructs M/n rows of every layer (tag_sfb_group_sync_sharded)"}
 
     # ---------------------------------------------------------------- e2e through host buffers
     dWh = [torch.empty(l["L"].M, l["L"].N, dtype=tdt[cfg.out_dtype]).pin_memory() for l in layers]

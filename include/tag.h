@@ -214,6 +214,12 @@ tag_status_t tag_sfb_group_sync(tag_sfb_group_t group, const void* const* X,
 tag_status_t tag_sfb_group_sync_sgd(tag_sfb_group_t group, const void* const* X,
                                     const void* const* dY, float* const* W, float* const* v,
                                     void* const* dW, tag_stream_t stream);
+/* Sharded form of tag_sfb_group_sync: dW_shard[i] is plans[i]'s row shard for this rank
+ * (tag_sfb_shard_rows). One fused launch when every plan takes the fused path and every shard is
+ * non-empty; otherwise one gather + per-plan reconstructions. */
+tag_status_t tag_sfb_group_sync_sharded(tag_sfb_group_t group, const void* const* X,
+                                        const void* const* dY, void* const* dW_shard,
+                                        tag_stream_t stream);
 /* Stage split, as for single plans: gather = a1 + a2 of every layer, reconstruct = a3 + a4. */
 tag_status_t tag_sfb_group_gather(tag_sfb_group_t group, const void* const* X,
                                   const void* const* dY, tag_stream_t stream);

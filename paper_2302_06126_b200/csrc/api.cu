@@ -880,6 +880,48 @@ tag_status_t tag_sfb_group_sync_sgd(tag_sfb_group_t g, const void* const* X, con
     return group_reconstruct(g, dWs, true, W, v, stream);
 }
 
+tag_status_t tag_sfb_group_sync_sharded(tag_sfb_group_t g, const void* const* X,
+                                        const void* const* dY, void* const* dW,
+                                        tag_stream_t stream) {
+    if (!g || !X || !dY || !dW)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync_sharded: NULL argument");
+    if (g->plans[0]->d.fuse_sgd)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync_sharded: fuse_sgd group");
+    const int count = static_cast<int>(g->plans.size());
+    bool fuse = true;
+    for (int i = 0; i < count; ++i) {
+        int64_t rb, rc;
+        shard_range(g->plans[i], g->plans[i]->comm->rank, &rb, &rc);
+        TAG_TRY(check_ptrs("tag_sfb_group_sync_sharded", {X[i], dY[i]}));
+        if (rc > 0) TAG_TRY(check_ptrs("tag_sfb_group_sync_sharded", {dW[i]}));
+        fuse = fuse && rc > 0 && fusable(g->plans[i], dW[i]);
+    }
+    TAG_TRY(set_device(g->plans[0]->comm));
+    TAG_TRY(check_async(g->plans[0]->comm));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (fuse) return fused_sync(g->plans.data(), count, X, dY, dW, false, nullptr, nullptr, s, true);
+    TAG_TRY(tag_sfb_group_gather(g, X, dY, stream));
+    for (int i = 0; i < count; ++i) {
+        tag_plan_s* p = g->plans[i];
+        int64_t rb, rc;
+        shard_range(p, p->comm->rank, &rb, &rc);
+        if (rc == 0) continue;
+        ReconArgs r{};
+        r.A = static_cast<const char*>(p->src_x) + rb * dtype_size(p->d.wire_dtype);
+        r.Bm = p->src_dy;
+        r.C = dW[i];
+        r.M = rc;
+        r.N = p->d.N;
+        r.K = p->K;
+        r.lda = p->d.M;
+        r.wire = p->d.wire_dtype;
+        r.out = p->d.out_dtype;
+        r.alpha = p->alpha;
+        TAG_TRY((p->use_tc && recon_tc_ok(r)) ? launch_recon_tc(r, s) : launch_recon_simt(r, s));
+    }
+    return TAG_OK;
+}
+
 tag_status_t tag_sfb_group_sync(tag_sfb_group_t g, const void* const* X, const void* const* dY,
                                 void* const* dW, tag_stream_t stream) {
     if (!g || !X || !dY || !dW) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync: NULL argument");

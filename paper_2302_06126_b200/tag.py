@@ -82,6 +82,7 @@ _SIGS = {
     "tag_sfb_select": ([_p(LayerDesc), _i, _p(Topology), _p(_i)], _st),
     "tag_sfb_group_create": ([_p(_vp), _i, _p(_vp)], _st),
     "tag_sfb_group_destroy": ([_vp], _st),
+    "tag_sfb_group_sync_sharded": ([_vp, _p(_vp), _p(_vp), _p(_vp), _vp], _st),
     "tag_sfb_group_sync": ([_vp, _p(_vp), _p(_vp), _p(_vp), _vp], _st),
     "tag_sfb_group_gather": ([_vp, _p(_vp), _p(_vp), _vp], _st),
     "tag_sfb_group_sync_sgd": ([_vp, _p(_vp), _p(_vp), _p(_vp), _p(_vp), _p(_vp), _vp], _st),
@@ -305,6 +306,15 @@ class SfbGroup:
     def sync(self, Xs, dYs, dWs, stream=None):
         _check(_lib.tag_sfb_group_sync(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"),
                                        self._ptrs(dWs, "dW"), _stream(stream)), "tag_sfb_group_sync")
+
+    def sync_sharded(self, Xs, dYs, dW_shards, stream=None):
+        ptrs = []
+        for p, t in zip(self.plans, dW_shards):
+            _, rc = p.shard_rows()
+            ptrs.append(_dev(t, p.out_torch, (rc, p.N), "dW_shard") if rc > 0 else _vp())
+        _check(_lib.tag_sfb_group_sync_sharded(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"),
+                                               (_vp * len(ptrs))(*ptrs), _stream(stream)),
+               "tag_sfb_group_sync_sharded")
 
     def sync_sgd(self, Xs, dYs, Ws, vs, dWs=None, stream=None):
         shapes = [(p.M, p.N) for p in self.plans]

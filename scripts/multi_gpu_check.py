@@ -170,6 +170,29 @@ def main():
         record(f"sharded_{M}x{N}", torch.equal(shard, full[rb:rb + rc]) and tiles_ok, rows=[rb, rc])
         plan.close()
 
+    # 10: sharded bucket == the rows of per-layer full syncs
+    specs = [(25088, 4096, 32, "relu", "masked_small"), (4096, 1000, 32, "relu", "softmax_onehot")]
+    plans, Xs, dYs, fulls, shards = [], [], [], [], []
+    for li, (M, N, B, xd, dyd) in enumerate(specs):
+        X, dY = synth.factors(2, 30 + li, rank, M, N, B, xd, dyd)
+        p = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32")
+        plans.append(p)
+        Xs.append(torch.from_numpy(X).to(torch.bfloat16).cuda())
+        dYs.append(torch.from_numpy(dY).to(torch.bfloat16).cuda())
+        fulls.append(torch.empty(M, N, device="cuda"))
+        p.sync(Xs[-1], dYs[-1], fulls[-1])
+        rb, rc = p.shard_rows()
+        shards.append(torch.empty(max(rc, 1), N, device="cuda")[:rc])
+    g = tag.SfbGroup(plans)
+    g.sync_sharded(Xs, dYs, shards)
+    torch.cuda.synchronize()
+    ok_sh = all(torch.equal(sh, f[p.shard_rows()[0]:p.shard_rows()[0] + p.shard_rows()[1]])
+                for p, sh, f in zip(plans, shards, fulls))
+    record("group_sharded", ok_sh)
+    g.close()
+    for p in plans:
+        p.close()
+
     # 7: selector identical on all ranks and equal to the oracle
     lays = [dict(M=L.M, N=L.N, B=L.B) for c in (2, 3, 4, 5) for L in synth.CONFIGS[c].layers]
     got = tag.select([dict(l, factor_dtype="bf16", grad_dtype="f32") for l in lays], n,
