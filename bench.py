@@ -239,9 +239,17 @@ def main():
             ent["W"], ent["v"] = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
         layers.append(ent)
     peaks, peak_src = load_peaks()
-    choices = tag.select([dict(M=l["L"].M, N=l["L"].N, B=l["L"].B, factor_dtype=cfg.wire_dtype,
-                               grad_dtype=cfg.out_dtype) for l in layers], n,
-                         900_000_000_000, int(peaks.get("bf16_tflops_sustained", 1400) * 1e12))
+    sel_layers = [dict(M=l["L"].M, N=l["L"].N, B=l["L"].B, factor_dtype=cfg.wire_dtype,
+                       grad_dtype=cfg.out_dtype) for l in layers]
+    choices = tag.select(sel_layers, n, 900_000_000_000,
+                         int(peaks.get("bf16_tflops_sustained", 1400) * 1e12))
+    # profiled selector (paper's profiler P:331-334): curves measured by scripts/profile_comm.py
+    choices_prof = None
+    prof_path = os.path.join(ROOT, "profiles", f"comm_n{n}.json")
+    if n > 1 and os.path.exists(prof_path):
+        prof = json.load(open(prof_path))
+        choices_prof = tag.select_profiled(sel_layers, n, prof["gather"], prof["allreduce"],
+                                           int(peaks.get("bf16_tflops_sustained", 1400) * 1e12))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     flush_rd = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -408,6 +416,8 @@ def main():
             "recon_tensor_frac": round(flops / (t_rec * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
             "allgather_busbw_GBps": round(ag / ((t_sync - t_rec) * 1e-3) / 1e9, 1) if n > 1 else None,
             "selector": {0: "allreduce", 1: "sfb", 2: "none"}[choices[i]],
+            "selector_profiled": ({0: "allreduce", 1: "sfb", 2: "none"}[choices_prof[i]]
+                                  if choices_prof else None),
             "gather": l["plan"].info()["gather"] + ("+multicast" if l["plan"].info()["multicast"] else "")}
     if group is not None and n > 1:
         t_gather = tdist.max_over_ranks(statistics.mean(staged_g_ms))
@@ -432,6 +442,7 @@ def main():
             td = tdist.max_over_ranks(statistics.median(t))
             per_layer[L.name]["dense_us"] = round(td * 1e3, 2)
             per_layer[L.name]["sfb_speedup_vs_dense"] = round(td / (per_layer[L.name]["sync_us"] / 1e3), 2)
+            per_layer[L.name]["measured_winner"] = "sfb" if per_layer[L.name]["sync_us"] < td * 1e3 else "allreduce"
 
     # ---------------------------------------------------------------- sharded variant (n > 1)
     # every rank still receives all factors but reconstructs only its

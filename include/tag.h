@@ -270,6 +270,31 @@ typedef struct {
 tag_status_t tag_sfb_select(const tag_layer_t* layers, int num_layers, const tag_topology_t* topo,
                             tag_choice_t* out);
 
+/* Profiled selector (the paper's profiler; SPEC fit_comm / predict S:197-214;
+ * SURVEY §8(f) rank 4): the two synchronisation costs are read from curves measured on the
+ * machine (e.g. scripts/profile_comm.py) instead of the analytic ring formula, so per-collective
+ * latency is part of the decision. Curve: count >= 2 points, bytes strictly increasing; the time
+ * at x is the piecewise-linear interpolation between consecutive points, extended by the first /
+ * last segment outside them, evaluated in integer ns with floor rounding and clamped
+ * at 0. Decision per layer (S = B(M+N)e_w, G = M N e_g):
+ *   SFB iff gather((n-1) S) + floor((n-1) 2MNB 1e9 / F) < allreduce(G)   [F = 0: no compute term]
+ * ties keep AllReduce; n = 1 -> NONE. Exact integer arithmetic (bit-identical on every rank and
+ * to oracle/selector.py). Limits (TAG_ERR_INVALID_ARG beyond): n <= 65536, M, N, B <= 2^24,
+ * curve ns <= 2^40, bytes <= 2^62. */
+typedef struct {
+    int count;
+    const uint64_t* bytes;
+    const uint64_t* ns;
+} tag_curve_t;
+typedef struct {
+    int n;
+    tag_curve_t gather;      /* x = bytes each rank receives: (n-1) * B(M+N) e_w */
+    tag_curve_t allreduce;   /* x = gradient bytes M N e_g */
+    uint64_t tensor_flops;   /* F; 0 drops the compute term */
+} tag_profiled_topology_t;
+tag_status_t tag_sfb_select_profiled(const tag_layer_t* layers, int num_layers,
+                                     const tag_profiled_topology_t* topo, tag_choice_t* out);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -118,3 +118,33 @@ def select_integer_form(layer, topo):
         lhs = n * mult * S
         rhs = 2 * (n - 1) * G
     return CHOICE_SFB if lhs < rhs else CHOICE_ALLREDUCE
+
+
+# ---------------------------------------------------------------------------------------------
+# Profiled selector (the paper's profiler: "Segmented linear regression models are built
+# for GRPC transfer and for AllReduce communication"; SPEC fit_comm S:197-205 realises it as exact
+# piecewise-linear interpolation between consecutive profiled sizes, extended by the first / last
+# segment). Times in integer ns with floor rounding, clamped at 0, so the library's integer
+# evaluation can be compared decision for decision.
+# ---------------------------------------------------------------------------------------------
+def curve_ns(points, x):
+    """points: [(bytes, ns), ...] with strictly increasing bytes (>= 2 points)."""
+    i = 0
+    while i + 2 < len(points) and x > points[i + 1][0]:
+        i += 1
+    (b0, t0), (b1, t1) = points[i], points[i + 1]
+    t = t0 + ((x - b0) * (t1 - t0)) // (b1 - b0)       # Python // is floor division
+    return max(t, 0)
+
+
+def select_profiled(layer, n, gather_pts, allreduce_pts, F=0):
+    """SFB iff gather((n-1) S) + floor((n-1) 2MNB 1e9 / F) < allreduce(G); ties -> AllReduce."""
+    if n <= 1:
+        return CHOICE_NONE
+    M, N, B, e_w, e_g = layer["M"], layer["N"], layer["B"], layer["e_w"], layer["e_g"]
+    S = B * (M + N) * e_w
+    G = M * N * e_g
+    t_sfb = curve_ns(gather_pts, (n - 1) * S)
+    if F:
+        t_sfb += ((n - 1) * 2 * M * N * B * 10 ** 9) // F
+    return CHOICE_SFB if t_sfb < curve_ns(allreduce_pts, G) else CHOICE_ALLREDUCE

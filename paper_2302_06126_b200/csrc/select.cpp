@@ -103,3 +103,74 @@ extern "C" tag_status_t tag_sfb_select(const tag_layer_t* layers, int num_layers
     }
     return TAG_OK;
 }
+
+namespace tag {
+namespace {
+
+// floor(a / b) for b > 0 (C++ division truncates toward zero)
+i128 floor_div(i128 a, i128 b) {
+    i128 q = a / b;
+    if ((a % b != 0) && (a < 0)) --q;
+    return q;
+}
+
+bool curve_ok(const tag_curve_t& c) {
+    if (c.count < 2 || !c.bytes || !c.ns) return false;
+    for (int i = 1; i < c.count; ++i)
+        if (c.bytes[i] <= c.bytes[i - 1]) return false;
+    for (int i = 0; i < c.count; ++i)      // bounds that keep every product below 2^127
+        if (c.bytes[i] > (1ull << 62) || c.ns[i] > (1ull << 40)) return false;
+    return true;
+}
+
+// piecewise-linear time in ns at x bytes, floor-rounded, clamped at 0
+i128 curve_ns(const tag_curve_t& c, i128 x) {
+    int i = 0;                                   // segment [i, i+1]
+    while (i + 2 < c.count && x > static_cast<i128>(c.bytes[i + 1])) ++i;
+    const i128 b0 = c.bytes[i], b1 = c.bytes[i + 1];
+    const i128 t0 = c.ns[i], t1 = c.ns[i + 1];
+    i128 t = t0 + floor_div((x - b0) * (t1 - t0), b1 - b0);
+    return t < 0 ? 0 : t;
+}
+
+}  // namespace
+}  // namespace tag
+
+extern "C" tag_status_t tag_sfb_select_profiled(const tag_layer_t* layers, int num_layers,
+                                                const tag_profiled_topology_t* topo,
+                                                tag_choice_t* out) {
+    using namespace tag;
+    if (num_layers < 0 || !topo || (num_layers > 0 && (!layers || !out)))
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_select_profiled: bad arguments");
+    if (topo->n < 1 || topo->n > 65536)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_select_profiled: n must be in [1, 65536]");
+    if (!curve_ok(topo->gather) || !curve_ok(topo->allreduce))
+        return fail(TAG_ERR_INVALID_ARG,
+                    "tag_sfb_select_profiled: curves need >= 2 points with increasing bytes");
+    for (int i = 0; i < num_layers; ++i) {
+        const tag_layer_t& L = layers[i];
+        if (L.M < 1 || L.N < 1 || L.B < 1 || L.M > (1ll << 24) || L.N > (1ll << 24) ||
+            L.B > (1ll << 24))
+            return fail(TAG_ERR_INVALID_ARG, "tag_sfb_select_profiled: layer dims out of range");
+        if ((L.factor_dtype != TAG_F32 && L.factor_dtype != TAG_BF16) ||
+            (L.grad_dtype != TAG_F32 && L.grad_dtype != TAG_BF16))
+            return fail(TAG_ERR_INVALID_ARG, "tag_sfb_select_profiled: unknown dtype");
+    }
+    const i128 n = topo->n;
+    const i128 F = static_cast<i128>(topo->tensor_flops);
+    for (int i = 0; i < num_layers; ++i) {
+        const tag_layer_t& L = layers[i];
+        if (n <= 1) {
+            out[i] = TAG_SYNC_NONE;
+            continue;
+        }
+        const i128 M = L.M, N = L.N, B = L.B;
+        const i128 S = B * (M + N) * static_cast<i128>(dtype_size(L.factor_dtype));
+        const i128 G = M * N * static_cast<i128>(dtype_size(L.grad_dtype));
+        i128 t_sfb = curve_ns(topo->gather, (n - 1) * S);
+        if (F > 0) t_sfb += floor_div((n - 1) * 2 * M * N * B * 1000000000, F);
+        const i128 t_ar = curve_ns(topo->allreduce, G);
+        out[i] = t_sfb < t_ar ? TAG_SYNC_SFB : TAG_SYNC_ALLREDUCE;
+    }
+    return TAG_OK;
+}

@@ -50,6 +50,16 @@ class LayerDesc(ctypes.Structure):
                 ("factor_dtype", ctypes.c_int), ("grad_dtype", ctypes.c_int)]
 
 
+class Curve(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int), ("bytes", ctypes.POINTER(ctypes.c_uint64)),
+                ("ns", ctypes.POINTER(ctypes.c_uint64))]
+
+
+class ProfiledTopology(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int), ("gather", Curve), ("allreduce", Curve),
+                ("tensor_flops", ctypes.c_uint64)]
+
+
 class Topology(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("link_bytes_per_s", ctypes.c_uint64),
                 ("tensor_flops", ctypes.c_uint64), ("rule", ctypes.c_int)]
@@ -80,6 +90,7 @@ _SIGS = {
     "tag_dense_allreduce": ([_vp, _vp, _vp], _st),
     "tag_sgd_step": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_select": ([_p(LayerDesc), _i, _p(Topology), _p(_i)], _st),
+    "tag_sfb_select_profiled": ([_p(LayerDesc), _i, _p(ProfiledTopology), _p(_i)], _st),
     "tag_sfb_group_create": ([_p(_vp), _i, _p(_vp)], _st),
     "tag_sfb_group_destroy": ([_vp], _st),
     "tag_sfb_group_sync_sharded": ([_vp, _p(_vp), _p(_vp), _p(_vp), _vp], _st),
@@ -349,4 +360,28 @@ def select(layers, n, link_bytes_per_s=900_000_000_000, tensor_flops=0, rule=RUL
     topo = Topology(n, link_bytes_per_s, tensor_flops, rule)
     out = (ctypes.c_int * max(1, len(layers)))()
     _check(_lib.tag_sfb_select(arr, len(layers), ctypes.byref(topo), out), "tag_sfb_select")
+    return [out[i] for i in range(len(layers))]
+
+
+def _curve(points):
+    pts = list(points)
+    b = (ctypes.c_uint64 * len(pts))(*[int(p[0]) for p in pts])
+    t = (ctypes.c_uint64 * len(pts))(*[int(p[1]) for p in pts])
+    return Curve(len(pts), b, t), (b, t)
+
+
+def select_profiled(layers, n, gather_points, allreduce_points, tensor_flops=0):
+    """Per-layer choice from measured cost curves [(bytes, ns), ...] (tag_sfb_select_profiled)."""
+    layers = list(layers)
+    arr = (LayerDesc * max(1, len(layers)))()
+    for i, L in enumerate(layers):
+        arr[i] = LayerDesc(L["M"], L["N"], L["B"], _DT_OF[L.get("factor_dtype", "bf16")],
+                           _DT_OF[L.get("grad_dtype", "f32")])
+    g, keep_g = _curve(gather_points)
+    a, keep_a = _curve(allreduce_points)
+    topo = ProfiledTopology(n, g, a, tensor_flops)
+    out = (ctypes.c_int * max(1, len(layers)))()
+    _check(_lib.tag_sfb_select_profiled(arr, len(layers), ctypes.byref(topo), out),
+           "tag_sfb_select_profiled")
+    del keep_g, keep_a
     return [out[i] for i in range(len(layers))]

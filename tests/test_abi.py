@@ -119,3 +119,34 @@ def test_no_gpu_means_loud_failure(tagmod):
     with pytest.raises(tagmod.TagError) as e:
         tagmod.Comm(1, 0, 0)
     assert e.value.status in (tagmod.ERR_CUDA, tagmod.ERR_INVALID_ARG)
+
+
+def test_select_profiled_bit_exact(tagmod, oracle_mod):
+    S = oracle_mod.selector
+    rs = np.random.default_rng(31)
+    dt = {2: "bf16", 4: "f32"}
+    for _ in range(300):
+        npts = int(rs.integers(2, 8))
+        def curve():
+            b = np.cumsum(rs.integers(1, 10 ** 8, npts)).tolist()
+            t = rs.integers(1000, 10 ** 7, npts).tolist()
+            return list(zip(b, t))
+        g, a = curve(), curve()
+        n = int(rs.integers(1, 17))
+        F = int(rs.choice([0, int(rs.integers(10 ** 12, 3 * 10 ** 15))]))
+        lays = [dict(M=int(rs.integers(1, 30000)), N=int(rs.integers(1, 30000)),
+                     B=int(rs.integers(1, 2048)), e_w=int(rs.choice([2, 4])),
+                     e_g=int(rs.choice([2, 4]))) for _ in range(4)]
+        got = tagmod.select_profiled([dict(M=l["M"], N=l["N"], B=l["B"], factor_dtype=dt[l["e_w"]],
+                                           grad_dtype=dt[l["e_g"]]) for l in lays], n, g, a, F)
+        want = [S.select_profiled(l, n, g, a, F) for l in lays]
+        assert got == want
+
+
+def test_select_profiled_errors(tagmod):
+    with pytest.raises(tagmod.TagError):
+        tagmod.select_profiled([dict(M=4, N=4, B=1)], 2, [(1, 1)], [(1, 1), (2, 2)])   # 1 point
+    with pytest.raises(tagmod.TagError):
+        tagmod.select_profiled([dict(M=4, N=4, B=1)], 2, [(2, 1), (1, 2)], [(1, 1), (2, 2)])
+    assert tagmod.select_profiled([dict(M=4, N=4, B=1)], 1, [(1, 1), (2, 2)],
+                                  [(1, 1), (2, 2)]) == [tagmod.SYNC_NONE]

@@ -261,3 +261,58 @@ def test_appendix_a_decision_table(oracle_mod):
         lay = dict(M=c["M"], N=c["N"], B=c["B"], e_w=c["e_w"], e_g=c["e_g"])
         topo = dict(n=c["n"], tau=c["tau"], F=c["F"], rule=c["rule"])
         assert name[S.select(lay, topo)] == c["expect"], c
+
+
+# ---------------------------------------------------------------------------------------------
+# Profiled selector (paper's profiler P:323-334; SPEC fit_comm S:197-205)
+# ---------------------------------------------------------------------------------------------
+def test_spec_fit_comm_interpolation(oracle_mod):
+    g = _golden("spec_fit_comm.json")
+    for x, want in g["queries"]:
+        assert oracle_mod.selector.curve_ns(g["points"], x) == want
+
+
+def test_curve_first_segment_and_clamp(oracle_mod):
+    S = oracle_mod.selector
+    pts = [(1000, 5000), (2000, 9000), (4000, 10000)]
+    assert S.curve_ns(pts, 500) == 3000          # extended below the first point
+    assert S.curve_ns(pts, 0) == 1000
+    assert S.curve_ns([(1000, 100), (2000, 5000)], 0) == 0      # clamped at 0
+    assert S.curve_ns(pts, 3000) == 9500         # second segment
+    assert S.curve_ns(pts, 8000) == 12000        # last segment's slope
+
+
+def test_profiled_reduces_to_ring_model(oracle_mod):
+    """Linear curves t = bytes / tau (gather) and t = 2(n-1)/n G / tau (ring AR), no latency: the
+    profiled rule decides like the analytic WIRE rule (F = 0) wherever it is not a tie."""
+    S = oracle_mod.selector
+    rs = np.random.default_rng(21)
+    tau = 10 ** 9                                 # 1 byte per ns
+    checked = 0
+    for _ in range(2000):
+        n = int(rs.integers(2, 17))
+        lay = dict(M=int(rs.integers(8, 5000)), N=int(rs.integers(8, 5000)),
+                   B=int(rs.integers(1, 300)), e_w=2, e_g=4)
+        gather = [(0, 0), (10 ** 12, 10 ** 12)]
+        ar = [(0, 0), (n * 10 ** 12, 2 * (n - 1) * 10 ** 12)]     # slope 2(n-1)/n
+        sfb_ns = (n - 1) * lay["B"] * (lay["M"] + lay["N"]) * 2
+        ar_exact = Fraction(2 * (n - 1) * lay["M"] * lay["N"] * 4, n)
+        if abs(sfb_ns - ar_exact) <= 1:
+            continue                              # floor rounding may flip exact ties
+        want = S.select(lay, dict(n=n, tau=tau, F=0, rule=S.RULE_WIRE))
+        assert S.select_profiled(lay, n, gather, ar) == want
+        checked += 1
+    assert checked > 1900
+
+
+def test_profiled_latency_flips_small_layers(oracle_mod):
+    """A fixed per-call latency on the gather (the measured NVLink push floor) turns tiny layers
+    to AllReduce that the bandwidth-only model sends to SFB — the reason for profiling."""
+    S = oracle_mod.selector
+    lay = dict(M=1024, N=1024, B=2, e_w=2, e_g=4)        # BERT-L pooler, n = 8
+    gather = [(0, 20000), (10 ** 9, 20000 + 10 ** 9 // 700)]      # 20 us + 700 GB/s
+    ar = [(0, 8000), (10 ** 9, 8000 + 10 ** 9 // 700)]            # 8 us + 700 GB/s
+    assert S.select(lay, dict(n=8, tau=900 * 10 ** 9, F=0)) == S.CHOICE_SFB
+    assert S.select_profiled(lay, 8, gather, ar) == S.CHOICE_ALLREDUCE
+    big = dict(M=25088, N=4096, B=32, e_w=2, e_g=4)        # VGG-19 fc6 stays SFB
+    assert S.select_profiled(big, 8, gather, ar) == S.CHOICE_SFB
