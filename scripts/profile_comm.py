@@ -78,7 +78,7 @@ if rank == 0:
            "allreduce": allreduce,
            "how": "scripts/profile_comm.py: one call after tag_comm_barrier, median of reps, max over ranks"}
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    path = os.path.join(ROOT, "profiles", f"comm_n{world}.json")
+    path = os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "profiles", f"comm_n{world}.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
     print(json.dumps(out))
