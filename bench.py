@@ -419,7 +419,7 @@ def main():
             "selector_profiled": ({0: "allreduce", 1: "sfb", 2: "none"}[choices_prof[i]]
                                   if choices_prof else None),
             "gather": l["plan"].info()["gather"] + ("+multicast" if l["plan"].info()["multicast"] else "")}
-    if group is not None and n > 1:
+    if group is not None and n > 1 and staged_g_ms:
         t_gather = tdist.max_over_ranks(statistics.mean(staged_g_ms))
         ag_all = sum((n - 1) * l["L"].B * (l["L"].M + l["L"].N) * ESIZE[cfg.wire_dtype] for l in layers)
         per_layer["bucket_gather_staged"] = {"us": round(t_gather * 1e3, 2),
