@@ -504,6 +504,43 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                         }
                         continue;
                     }
+                    if constexpr (SGD) {
+                        if (full) {
+                            // E2 fast path: all 16 loads of W and v in flight before any math
+                            // (the per-row load -> update -> store chain would serialise on the
+                            // HBM latency 8 times per chunk)
+                            float4* wp4 = reinterpret_cast<float4*>(Wp + off0);
+                            float4* vp4 = reinterpret_cast<float4*>(Vp + off0);
+                            const int64_t gstep = step / 4;
+                            float4 wv[8], vv[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                wv[i] = __ldcs(wp4 + i * gstep);
+                                vv[i] = __ldcs(vp4 + i * gstep);
+                            }
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                uint32_t dw[4];
+                                ptx::ld_shared_v4(sq + i * 512 + ((i & 1) ? sw1 : sw0), dw[0],
+                                                  dw[1], dw[2], dw[3]);
+                                float* wf = reinterpret_cast<float*>(&wv[i]);
+                                float* vf = reinterpret_cast<float*>(&vv[i]);
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    // E2 (R14): g = dW + wd*W ; v = mu*v + g ; W -= lr*v
+                                    const float g = __fadd_rn(__uint_as_float(dw[e]), __fmul_rn(wd, wf[e]));
+                                    vf[e] = __fadd_rn(__fmul_rn(mu, vf[e]), g);
+                                    wf[e] = __fsub_rn(wf[e], __fmul_rn(lr, vf[e]));
+                                }
+                                __stcs(wp4 + i * gstep, wv[i]);
+                                __stcs(vp4 + i * gstep, vv[i]);
+                                if (Cp != nullptr)
+                                    __stcs(reinterpret_cast<uint4*>(Cp + (off0 + i * step) * ESZ),
+                                           make_uint4(dw[0], dw[1], dw[2], dw[3]));
+                            }
+                            continue;
+                        }
+                    }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const int r = 4 * i + sub;
