@@ -295,6 +295,34 @@ typedef struct {
 tag_status_t tag_sfb_select_profiled(const tag_layer_t* layers, int num_layers,
                                      const tag_profiled_topology_t* topo, tag_choice_t* out);
 
+/* General SFB cut ILP: for one gradient tensor (g, l) of a
+ * replicated op group V, choose which ops to duplicate (alpha_i) so as to
+ *   min (D-1) sum_i alpha_i T_i + D(D-1) sum_{(j,i) in E} b_ji L_ji / tau - 2 alpha_g (D-1)/D L_gl / tau
+ *   s.t. alpha_k <= sum_{(k,i) in E} alpha_i (k != l),  b_ji >= alpha_i - alpha_j,  binary.
+ * Readings (DESIGN R20): alpha_l = 1 and T_l excluded; edge_src = -1 marks a
+ * producer outside the group (alpha 0); edges into l are not cut candidates; b_ji = max(0,
+ * alpha_i - alpha_j). Solved exactly in polynomial time as ONE s-t minimum cut ("similar to the
+ * min-cut problem"; derivation in csrc/ilp.cpp) with integer costs (T in ns, L in
+ * bytes, tau in bytes/s); among optimal assignments the one duplicating the fewest ops is
+ * returned (it is unique), so an objective of exactly 0 keeps the all-zero one. The
+ * Fig. 5 MatMul instance reduces to tag_sfb_select's TAG_RULE_PAPER_ILP. Host only.
+ * Errors: TAG_ERR_INVALID_ARG (bad indices, cycles, D outside [1, 1024], tau 0, num_ops outside
+ * [2, 64], > 4096 edges), TAG_ERR_UNSUPPORTED (T > 2^40 ns or bytes > 2^50: 127-bit range). */
+typedef struct {
+    int num_ops;                 /* |V|, 2..64; ops are 0..num_ops-1                         */
+    int l, g;                    /* the optimizer op and the op producing its gradient        */
+    const uint64_t* op_ns;       /* T_i: compute time of op i at the per-replica batch, ns    */
+    int num_edges;
+    const int* edge_src;         /* j: producer op, or -1 for a producer outside the group    */
+    const int* edge_dst;         /* i: consumer op (an op of the group)                       */
+    const uint64_t* edge_bytes;  /* L_ji                                                      */
+    uint64_t grad_bytes;         /* L_gl                                                      */
+    int D;                       /* replicas                                                  */
+    uint64_t tau;                /* bottleneck bandwidth, bytes/s                             */
+} tag_sfb_ilp_t;
+/* alpha_out[num_ops]: 1 = duplicate; objective_s: the optimum in seconds (0 for all-zero). */
+tag_status_t tag_sfb_ilp_solve(const tag_sfb_ilp_t* inst, uint8_t* alpha_out, double* objective_s);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -148,3 +148,62 @@ def select_profiled(layer, n, gather_pts, allreduce_pts, F=0):
     if F:
         t_sfb += ((n - 1) * 2 * M * N * B * 10 ** 9) // F
     return CHOICE_SFB if t_sfb < curve_ns(allreduce_pts, G) else CHOICE_ALLREDUCE
+
+
+# ---------------------------------------------------------------------------------------------
+# The general SFB ILP (SPEC solve_bruteforce S:490-495), by exhaustive enumeration.
+#   min (D-1) sum_i a_i T_i + D(D-1) sum_{(j,i) in E} b_ji L_ji / tau - 2 a_g (D-1)/D L_gl / tau
+#   s.t. a_k <= sum_{(k,i) in E} a_i  for k in V \ {l};  b_ji >= a_i - a_j;  a, b binary.
+# Readings (DESIGN R20): a_l = 1 and T_l excluded; producers outside the group have
+# a = 0 (src = -1); edges into l are not cut candidates (l runs on every replica either way; the
+# gradient's own synchronisation is the third term); b_ji = max(0, a_i - a_j), the cheapest
+# feasible cut. Ties: the assignment duplicating the fewest ops wins (then the lexicographically
+# smallest a vector, which ilp_bruteforce reports as `ambiguous` — the minimal optimum is unique
+# because minimum cuts form a lattice, DESIGN R20).
+# ---------------------------------------------------------------------------------------------
+def ilp_eval(inst, alpha):
+    """Exact objective (Fraction seconds) of assignment `alpha` (list of 0/1, alpha[l] == 1), or
+    None if it violates constraint 1."""
+    V, l, g = inst["num_ops"], inst["l"], inst["g"]
+    D, tau = inst["D"], inst["tau"]
+    edges = inst["edges"]                     # [(src or -1, dst, bytes)]
+    for k in range(V):
+        if k == l or not alpha[k]:
+            continue
+        if not any(alpha[i] for (j, i, _) in edges if j == k):
+            return None
+    obj = Fraction(0)
+    for i in range(V):
+        if i != l and alpha[i]:
+            obj += Fraction((D - 1) * inst["op_ns"][i], 10 ** 9)
+    for (j, i, L) in edges:
+        if i == l:
+            continue
+        aj = alpha[j] if j >= 0 else 0
+        if alpha[i] - aj > 0:
+            obj += Fraction(D * (D - 1) * L, tau)
+    if alpha[g]:
+        obj -= 2 * Fraction(D - 1, D) * Fraction(inst["grad_bytes"], tau)
+    return obj
+
+
+def ilp_bruteforce(inst):
+    """(objective, alpha, ambiguous) minimising over all 2^(|V|-1) assignments with alpha_l = 1.
+    `ambiguous` is True when another optimum duplicates equally few ops."""
+    V, l = inst["num_ops"], inst["l"]
+    free = [k for k in range(V) if k != l]
+    best, ambiguous = None, False
+    for mask in range(1 << len(free)):
+        alpha = [0] * V
+        alpha[l] = 1
+        for b, k in enumerate(free):
+            alpha[k] = (mask >> b) & 1
+        obj = ilp_eval(inst, alpha)
+        if obj is None:
+            continue
+        key = (obj, sum(alpha))
+        if best is None or key < (best[0], sum(best[1])):
+            best, ambiguous = (obj, alpha), False
+        elif key == (best[0], sum(best[1])):
+            ambiguous = True
+    return best[0], best[1], ambiguous

@@ -60,6 +60,14 @@ class ProfiledTopology(ctypes.Structure):
                 ("tensor_flops", ctypes.c_uint64)]
 
 
+class IlpInstance(ctypes.Structure):
+    _fields_ = [("num_ops", ctypes.c_int), ("l", ctypes.c_int), ("g", ctypes.c_int),
+                ("op_ns", ctypes.POINTER(ctypes.c_uint64)), ("num_edges", ctypes.c_int),
+                ("edge_src", ctypes.POINTER(ctypes.c_int)), ("edge_dst", ctypes.POINTER(ctypes.c_int)),
+                ("edge_bytes", ctypes.POINTER(ctypes.c_uint64)), ("grad_bytes", ctypes.c_uint64),
+                ("D", ctypes.c_int), ("tau", ctypes.c_uint64)]
+
+
 class Topology(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("link_bytes_per_s", ctypes.c_uint64),
                 ("tensor_flops", ctypes.c_uint64), ("rule", ctypes.c_int)]
@@ -91,6 +99,7 @@ _SIGS = {
     "tag_sgd_step": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_select": ([_p(LayerDesc), _i, _p(Topology), _p(_i)], _st),
     "tag_sfb_select_profiled": ([_p(LayerDesc), _i, _p(ProfiledTopology), _p(_i)], _st),
+    "tag_sfb_ilp_solve": ([_p(IlpInstance), _p(ctypes.c_uint8), _p(ctypes.c_double)], _st),
     "tag_sfb_group_create": ([_p(_vp), _i, _p(_vp)], _st),
     "tag_sfb_group_destroy": ([_vp], _st),
     "tag_sfb_group_sync_sharded": ([_vp, _p(_vp), _p(_vp), _p(_vp), _vp], _st),
@@ -385,3 +394,20 @@ def select_profiled(layers, n, gather_points, allreduce_points, tensor_flops=0):
            "tag_sfb_select_profiled")
     del keep_g, keep_a
     return [out[i] for i in range(len(layers))]
+
+
+def ilp_solve(inst):
+    """General SFB cut ILP (tag_sfb_ilp_solve). inst: dict(num_ops, l, g, op_ns[list], edges
+    [(src or -1, dst, bytes)], grad_bytes, D, tau). Returns (alpha list, objective seconds)."""
+    V, E = inst["num_ops"], inst["edges"]
+    op_ns = (ctypes.c_uint64 * V)(*inst["op_ns"])
+    ne = max(1, len(E))
+    src = (ctypes.c_int * ne)(*[e[0] for e in E])
+    dst = (ctypes.c_int * ne)(*[e[1] for e in E])
+    byt = (ctypes.c_uint64 * ne)(*[e[2] for e in E])
+    c = IlpInstance(V, inst["l"], inst["g"], op_ns, len(E), src, dst, byt, inst["grad_bytes"],
+                    inst["D"], inst["tau"])
+    alpha = (ctypes.c_uint8 * V)()
+    obj = ctypes.c_double()
+    _check(_lib.tag_sfb_ilp_solve(ctypes.byref(c), alpha, ctypes.byref(obj)), "tag_sfb_ilp_solve")
+    return [alpha[i] for i in range(V)], obj.value
