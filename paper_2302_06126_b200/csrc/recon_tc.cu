@@ -56,7 +56,8 @@ struct Cfg {
     static constexpr int A_BYTES = (BM / 64) * CHUNK_BYTES;
     static constexpr int B_BYTES = (BN / CTAS / 64) * CHUNK_BYTES;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = BN == 256 ? 6 : 8;
+    // pairs: 8 stages (VGG bucket at K = 256: 104 -> 99 us vs 6; 9-10 no better)
+    static constexpr int STAGES = CTAS == 2 ? 8 : (BN == 256 ? 6 : 8);
     static constexpr int EPI_BYTES = NUM_EPI_WARPS * EPI_BUF_BYTES;
     static constexpr int BAR_BYTES = 256;
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
@@ -392,7 +393,7 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
         constexpr int COLS_PER_CHUNK = 128 / ESZ;               // 128 bytes of output per row
         constexpr int CHUNKS = (BN / 2) / COLS_PER_CHUNK;
         constexpr int VEC = 16 / ESZ;                           // output elements per 16 B
-        constexpr int PAIR = OUT_BF16 ? 1 : 2;                  // chunks staged per round
+        constexpr int PAIR = OUT_BF16 || SGD ? 1 : 2;           // chunks staged per round
         const int sub = lane >> 3;               // row within a 4-row group (write-out phase)
         const int cj = lane & 7;                 // 16-byte column slot (write-out phase)
         int acc = 0;

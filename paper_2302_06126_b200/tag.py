@@ -11,7 +11,8 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtag.so")
+# TAG_LIB_PATH: load an experimental build instead (diagnostics/sweeps only)
+LIB_PATH = os.environ.get("TAG_LIB_PATH") or os.path.join(_HERE, "libtag.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libtag.so not built ({LIB_PATH}); run __graft_entry__.build() or "

@@ -28,6 +28,7 @@ for nv in (1, 2, 4, 8):
     ts = []
     for it in range(13):
         flush.zero_()
+        flush.sum()            # leave L2 holding clean lines (no write-back inside the timing)
         torch.cuda._sleep(1_000_000)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
