@@ -7,7 +7,8 @@ use is the seeded input generator in paper_2302_06126_b200/synth.py, which holds
 method's arithmetic.
 
 Contents
-  tag_oracle.c  fp64 dense route, SFB route, per-entry sums, SGD-momentum, RNE bf16 cast (plain C)
+  tag_oracle.c  fp64 dense route, SFB route, per-entry sums, bias gradient (both routes),
+                SGD-momentum, RNE bf16 cast (plain C)
   selector.py   exact-integer / Fraction selector, byte counts, ring-AllReduce and ILP formulas
 
 Parity status: every function here is pinned by tests/test_oracle.py against values the paper or
@@ -56,6 +57,10 @@ def _load():
         lib.oracle_sgd_momentum.restype = None
         lib.oracle_cast_bf16.argtypes = [i64, p, p]
         lib.oracle_cast_bf16.restype = None
+        for name in ("oracle_dense_bias_sum", "oracle_sfb_bias_sum"):
+            fn = getattr(lib, name)
+            fn.argtypes = [i64, i64, i64, p, p]
+            fn.restype = None
         _lib = lib
     return _lib
 
@@ -135,3 +140,27 @@ def bf16_bits_to_f64(bits):
     """Exact value of bf16 bit patterns (a bf16 is the top half of an fp32)."""
     b = np.ascontiguousarray(bits, dtype=np.uint16).astype(np.uint32) << 16
     return b.view(np.float32).astype(np.float64)
+
+
+def _bias(name, dY):
+    dY = _f64(dY)
+    n, B, N = dY.shape
+    out = np.empty(N, dtype=np.float64)
+    getattr(_load(), name)(n, B, N, _ptr(dY), _ptr(out))
+    return out
+
+
+def dense_bias_sum(dY):
+    """S_b = sum_r sum_b dY_r[b] (per-replica bias gradients, rank-order sum). dY: (n, B, N)."""
+    return _bias("oracle_dense_bias_sum", dY)
+
+
+def sfb_bias_sum(dY):
+    """S_b = sum_k dY_all[k] (column sums of the gathered dY_all)."""
+    return _bias("oracle_sfb_bias_sum", dY)
+
+
+def sfb_bias(dY):
+    """db = S_b / (nB) by the SFB route."""
+    n, B, _ = np.shape(dY)
+    return sfb_bias_sum(dY) / float(n * B)

@@ -155,3 +155,35 @@ void oracle_cast_bf16(int64_t len, const float* in, uint16_t* out)
 {
     for (int64_t i = 0; i < len; ++i) out[i] = rne_bf16(in[i]);
 }
+
+/* ---------------------------------------------------------------------------------------------
+ * Bias gradient of the Dense layer y = x W + b (R17). The sufficient factors "can
+ * generate a gradient tensor, usually by an outer product": the bias is the weight
+ * of a constant input 1, so its gradient is the outer product of the ones vector with dY, i.e.
+ * the column sums of dY — it needs only the factor dY that SFB already broadcasts.
+ * Dense route (AllReduce of per-replica bias gradients):
+ *   db_r[j] = sum_{b<B} dY_r[b][j];   S_b[j] = sum_{r<n} db_r[j]   (rank order)
+ * SFB route (from the gathered dY_all):
+ *   S_b[j] = sum_{k<K} dY_all[k][j]                                  (k order)
+ * Both return the unscaled sum (length N); the scale is alpha = 1/(nB) as for dW (R1).
+ * ------------------------------------------------------------------------------------------- */
+void oracle_dense_bias_sum(int64_t n, int64_t B, int64_t N, const double* dY, double* S)
+{
+    for (int64_t j = 0; j < N; ++j) {
+        double s = 0.0;
+        for (int64_t r = 0; r < n; ++r) {
+            double g = 0.0;
+            for (int64_t b = 0; b < B; ++b) g += dY[(r * B + b) * N + j];
+            s += g;
+        }
+        S[j] = s;
+    }
+}
+
+void oracle_sfb_bias_sum(int64_t n, int64_t B, int64_t N, const double* dY_all, double* S)
+{
+    const int64_t K = n * B;
+    for (int64_t j = 0; j < N; ++j) S[j] = 0.0;
+    for (int64_t k = 0; k < K; ++k)
+        for (int64_t j = 0; j < N; ++j) S[j] += dY_all[k * N + j];
+}

@@ -316,3 +316,42 @@ def test_profiled_latency_flips_small_layers(oracle_mod):
     assert S.select_profiled(lay, 8, gather, ar) == S.CHOICE_ALLREDUCE
     big = dict(M=25088, N=4096, B=32, e_w=2, e_g=4)        # VGG-19 fc6 stays SFB
     assert S.select_profiled(big, 8, gather, ar) == S.CHOICE_SFB
+
+
+# ------------------------------------------------------------------ bias gradient (R17)
+def test_bias_dense_equals_sfb_and_numpy(oracle_mod):
+    """Lossless for the bias too: the AllReduce route (per-replica column sums, rank order) and
+    the SFB route (column sums of dY_all) agree, exactly on integers; numpy's sum pins both."""
+    rs = np.random.default_rng(51)
+    for n, B, N in ((1, 1, 1), (2, 4, 32), (3, 5, 17), (8, 32, 1000)):
+        dYi = rs.integers(-3, 4, (n, B, N)).astype(np.float64)
+        assert np.array_equal(oracle_mod.dense_bias_sum(dYi), oracle_mod.sfb_bias_sum(dYi))
+        assert np.array_equal(oracle_mod.sfb_bias_sum(dYi), dYi.sum(axis=(0, 1)))
+        dYr = rs.standard_normal((n, B, N))
+        np.testing.assert_allclose(oracle_mod.dense_bias_sum(dYr), oracle_mod.sfb_bias_sum(dYr),
+                                   rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(oracle_mod.sfb_bias(dYr), dYr.reshape(n * B, N).mean(axis=0),
+                                   rtol=1e-13, atol=1e-13)
+
+
+def test_bias_is_weight_gradient_of_a_constant_input(oracle_mod):
+    """the gradient is an outer product of the factors. Appending a constant-1 column
+    to x makes the bias a row of W, and its gradient row equals the SFB bias sum."""
+    rs = np.random.default_rng(52)
+    n, B, M, N = 3, 4, 6, 9
+    X = rs.integers(-3, 4, (n, B, M)).astype(np.float64)
+    dY = rs.integers(-3, 4, (n, B, N)).astype(np.float64)
+    Xa = np.concatenate([X, np.ones((n, B, 1))], axis=2)
+    S = oracle_mod.sfb_sum(Xa, dY)
+    assert np.array_equal(S[M], oracle_mod.sfb_bias_sum(dY))
+
+
+def test_bias_fractions_and_ones(oracle_mod):
+    """Exact rationals on a tiny case; dY = 1 gives db = 1 after the 1/(nB) scale."""
+    n, B, N = 2, 3, 4
+    vals = [[[Fraction(1, 1 + r + b + j) for j in range(N)] for b in range(B)] for r in range(n)]
+    want = [sum(vals[r][b][j] for r in range(n) for b in range(B)) for j in range(N)]
+    got = oracle_mod.sfb_bias_sum(np.array(vals, dtype=np.float64))
+    for j in range(N):
+        assert abs(Fraction(got[j]) - want[j]) <= Fraction(1, 10 ** 14)
+    assert np.array_equal(oracle_mod.sfb_bias(np.ones((n, B, N))), np.ones(N))
