@@ -5,7 +5,7 @@
  * Deployment", arXiv 2302.06126).
  *
  * Citations: P:n = line n of the paper's LaTeX source; S:n = line n of SPEC.md.
- * DESIGN.md lists every reading taken where the paper is silent (R1..R19).
+ * DESIGN.md lists every reading taken where the paper is silent (R1..R20).
  *
  * The method (Fig. "fig:sfb_impl"): n data-parallel replicas of a Dense
  * layer with weight W (M x N; M = input features = the paper's H1, N = output features = H2) each
@@ -192,6 +192,17 @@ tag_status_t tag_sfb_shard_rows(tag_sfb_plan_t plan, int rank, int64_t* row_begi
 tag_status_t tag_sfb_sync_sharded(tag_sfb_plan_t plan, const void* X, const void* dY,
                                   void* dW_shard, tag_stream_t stream);
 
+/* Bias gradient of the layer (y = x W + b; DESIGN R17): db = alpha * sum_k dY_all[k][:], the
+ * column sums of the gathered output gradients — the bias is the weight of a constant input, so
+ * its gradient is the outer product of the ones vector with the factor dY that SFB already
+ * broadcasts; no communication. Reads the dY_all of this plan's most
+ * recent synchronisation on `stream` (tag_sfb_sync, _sgd, _sharded, _gather, or a group call
+ * containing the plan); at n = 1 without a cast that is the caller's dY, which must still be
+ * valid. db_out: N elements of out_dtype (device), overwritten; bitwise identical on every rank
+ * (fixed summation order, no atomics). Not collective. Errors: TAG_ERR_INVALID_ARG (NULL, or no
+ * factors gathered yet). */
+tag_status_t tag_sfb_bias_grad(tag_sfb_plan_t plan, void* db_out, tag_stream_t stream);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Buckets: several layers synchronised together                                             */
 /* ------------------------------------------------------------------------------------------ */
@@ -225,6 +236,9 @@ tag_status_t tag_sfb_group_gather(tag_sfb_group_t group, const void* const* X,
                                   const void* const* dY, tag_stream_t stream);
 tag_status_t tag_sfb_group_reconstruct(tag_sfb_group_t group, void* const* dW,
                                        tag_stream_t stream);
+/* tag_sfb_bias_grad of every plan of the group in ONE launch: db[i] (N_i elements, out_dtype). */
+tag_status_t tag_sfb_group_bias_grad(tag_sfb_group_t group, void* const* db,
+                                     tag_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------ */
 /* Dense-gradient baseline ("Replicate with AllReduce")                 */

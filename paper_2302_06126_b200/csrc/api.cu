@@ -596,6 +596,14 @@ tag_status_t tag_sfb_sync_sgd(tag_sfb_plan_t p, const void* X, const void* dY, f
     return do_recon(p, dW_out, true, W, v, p->K, p->alpha, s);
 }
 
+tag_status_t tag_sfb_bias_grad(tag_sfb_plan_t p, void* db_out, tag_stream_t stream) {
+    if (!p || !db_out) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_bias_grad: NULL argument");
+    if (!p->src_dy) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_bias_grad: no factors gathered on this plan yet");
+    TAG_TRY(set_device(p->comm));
+    BiasArgs a{p->src_dy, db_out, p->K, p->d.N, p->d.wire_dtype, p->d.out_dtype, p->alpha};
+    return launch_bias_grad(&a, 1, reinterpret_cast<cudaStream_t>(stream));
+}
+
 tag_status_t tag_sfb_shard_rows(tag_sfb_plan_t p, int rank, int64_t* row_begin, int64_t* row_count) {
     if (!p || !row_begin || !row_count) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_shard_rows: NULL argument");
     if (rank < 0 || rank >= p->d.n) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_shard_rows: bad rank");
@@ -853,6 +861,21 @@ tag_status_t tag_sfb_group_reconstruct(tag_sfb_group_t g, void* const* dW, tag_s
     if (g->plans[0]->d.fuse_sgd)
         return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_reconstruct: fuse_sgd group, use sync_sgd");
     return group_reconstruct(g, dW, false, nullptr, nullptr, stream);
+}
+
+tag_status_t tag_sfb_group_bias_grad(tag_sfb_group_t g, void* const* db, tag_stream_t stream) {
+    if (!g || !db) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_bias_grad: NULL argument");
+    BiasArgs a[MAX_GROUP];
+    const int count = static_cast<int>(g->plans.size());
+    for (int i = 0; i < count; ++i) {
+        tag_plan_s* p = g->plans[i];
+        if (!db[i]) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_bias_grad: NULL db entry");
+        if (!p->src_dy)
+            return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_bias_grad: no factors gathered yet");
+        a[i] = BiasArgs{p->src_dy, db[i], p->K, p->d.N, p->d.wire_dtype, p->d.out_dtype, p->alpha};
+    }
+    TAG_TRY(set_device(g->plans[0]->comm));
+    return launch_bias_grad(a, count, reinterpret_cast<cudaStream_t>(stream));
 }
 
 tag_status_t tag_sfb_group_sync_sgd(tag_sfb_group_t g, const void* const* X, const void* const* dY,

@@ -86,6 +86,17 @@ tag_status_t launch_push_gather_group(const void* dc, const PushSegment* seg, in
                                       tag_dtype_t in, tag_dtype_t wire, int max_ctas,
                                       cudaStream_t s);
 
+// ------------------------------------------------------------------ bias gradient (R17)
+struct BiasArgs {
+    const void* dy;        // dY_all (K x N, wire dtype)
+    void* db;              // N, out dtype
+    int64_t K, N;
+    tag_dtype_t wire, out;
+    float alpha;
+};
+// db = alpha * column sums of dY_all for 1..MAX_GROUP layers in one launch (bias.cu)
+tag_status_t launch_bias_grad(const BiasArgs* a, int count, cudaStream_t s);
+
 // ------------------------------------------------------------------ unfused SGD
 tag_status_t launch_sgd(const float* dW, float* W, float* V, int64_t len, float lr, float mu,
                         float wd, cudaStream_t s);

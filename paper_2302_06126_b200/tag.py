@@ -91,6 +91,7 @@ _SIGS = {
     "tag_sfb_sync": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_gather": ([_vp, _vp, _vp, _vp], _st),
     "tag_sfb_reconstruct": ([_vp, _vp, _vp], _st),
+    "tag_sfb_bias_grad": ([_vp, _vp, _vp], _st),
     "tag_sfb_sync_sgd": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_sync_host": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_shard_rows": ([_vp, _i, _p(ctypes.c_int64), _p(ctypes.c_int64)], _st),
@@ -108,6 +109,7 @@ _SIGS = {
     "tag_sfb_group_gather": ([_vp, _p(_vp), _p(_vp), _vp], _st),
     "tag_sfb_group_sync_sgd": ([_vp, _p(_vp), _p(_vp), _p(_vp), _p(_vp), _p(_vp), _vp], _st),
     "tag_sfb_group_reconstruct": ([_vp, _p(_vp), _vp], _st),
+    "tag_sfb_group_bias_grad": ([_vp, _p(_vp), _vp], _st),
 }
 for _name, (_args, _res) in _SIGS.items():
     _fn = getattr(_lib, _name)
@@ -246,6 +248,12 @@ class SfbPlan:
                                         _stream(stream)), "tag_sfb_reconstruct")
         return dW
 
+    def bias_grad(self, db, stream=None):
+        """db <- alpha * column sums of the dY_all of this plan's latest synchronisation."""
+        _check(_lib.tag_sfb_bias_grad(self._h, _dev(db, self.out_torch, (self.N,), "db"),
+                                      _stream(stream)), "tag_sfb_bias_grad")
+        return db
+
     def sync_sgd(self, X, dY, W, v, dW=None, stream=None):
         x, dy = self._xy(X, dY)
         shape = (self.M, self.N)
@@ -352,6 +360,12 @@ class SfbGroup:
     def reconstruct(self, dWs, stream=None):
         _check(_lib.tag_sfb_group_reconstruct(self._h, self._ptrs(dWs, "dW"), _stream(stream)),
                "tag_sfb_group_reconstruct")
+
+    def bias_grad(self, dbs, stream=None):
+        ptrs = [_dev(t, p.out_torch, (p.N,), "db") for p, t in zip(self.plans, dbs)]
+        assert len(ptrs) == len(self.plans), "db: one tensor per plan"
+        _check(_lib.tag_sfb_group_bias_grad(self._h, (_vp * len(ptrs))(*ptrs), _stream(stream)),
+               "tag_sfb_group_bias_grad")
 
     def close(self):
         if self._h:

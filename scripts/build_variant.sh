@@ -12,7 +12,7 @@ make -C "$csrc" -s
 nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC,-fvisibility=hidden \
   --expt-relaxed-constexpr -I$nccl/include -I$root/include "$@" -c "$csrc/recon_tc.cu" -o "$root/build_exp/recon_tc_$name.o"
 objs=""
-for o in api recon_simt pack_sgd push_gather select ilp; do objs="$objs $csrc/$o.o"; done
+for o in api recon_simt pack_sgd push_gather bias select ilp; do objs="$objs $csrc/$o.o"; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$root/build_exp/libtag_$name.so" $objs \
   "$root/build_exp/recon_tc_$name.o" -cudart static -L$nccl/lib -l:libnccl.so.2 -Xlinker -rpath,$nccl/lib
 echo "built build_exp/libtag_$name.so"

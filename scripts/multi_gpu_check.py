@@ -11,7 +11,8 @@ gradients"):
   4. the dense baseline (local GEMM + AllReduce with PreMulSum 1/(nB)) agrees with SFB;
   5. fp32 toy config (64x32, B=4) <= 1e-5; fp32 -> bf16 wire (pack + in-place gather);
   6. fused SGD-momentum: identical W, v on every rank and equal to the unfused path;
-  7. selector decisions identical on every rank and equal to the oracle's.
+  7. selector decisions identical on every rank and equal to the oracle's;
+  11. the bias gradient from the gathered dY_all: bit-exact on integers, identical on all ranks.
 Rank 0 prints one JSON line with the results; exit code 0 iff every check passed.
 """
 import hashlib
@@ -189,6 +190,35 @@ def main():
     ok_sh = all(torch.equal(sh, f[p.shard_rows()[0]:p.shard_rows()[0] + p.shard_rows()[1]])
                 for p, sh, f in zip(plans, shards, fulls))
     record("group_sharded", ok_sh)
+    g.close()
+    for p in plans:
+        p.close()
+
+    # 11: bias gradient from the gathered dY_all (R17): integer bucket bit-exact vs the oracle,
+    #     identical on every rank, group launch == per-plan launch
+    specs = [(520, 264, 24, "int3", "int3"), (4096, 1000, 32, "int3", "int3")]
+    plans, Xs, dYs, dWs = [], [], [], []
+    for li, (M, N, B, xd, dyd) in enumerate(specs):
+        X, dY = synth.factors(62, li, rank, M, N, B, xd, dyd)
+        plans.append(tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32"))
+        Xs.append(torch.from_numpy(X).to(torch.bfloat16).cuda())
+        dYs.append(torch.from_numpy(dY).to(torch.bfloat16).cuda())
+        dWs.append(torch.empty(M, N, device="cuda"))
+    g = tag.SfbGroup(plans)
+    g.sync(Xs, dYs, dWs)
+    dbs = [torch.full((p.N,), float("nan"), device="cuda") for p in plans]
+    g.bias_grad(dbs)
+    per = [torch.empty((p.N,), device="cuda") for p in plans]
+    for p, d in zip(plans, per):
+        p.bias_grad(d)
+    torch.cuda.synchronize()
+    okb = all(torch.equal(a, b) for a, b in zip(dbs, per))
+    for li, (M, N, B, xd, dyd) in enumerate(specs):
+        _, dYall = synth.all_factors(62, li, n, M, N, B, xd, dyd)
+        want = oracle.sfb_bias_sum(dYall).astype(np.float32) * np.float32(1.0 / (n * B))
+        okb = okb and np.array_equal(dbs[li].cpu().numpy().view(np.uint32), want.view(np.uint32))
+    hashes = tdist.all_gather_object("".join(digest(d) for d in dbs))
+    record("bias_grad", okb and len(set(hashes)) == 1)
     g.close()
     for p in plans:
         p.close()

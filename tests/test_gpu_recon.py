@@ -341,3 +341,82 @@ def test_group_sgd_equals_per_plan(tag, comm1):
     g.close()
     for p in plans:
         p.close()
+
+
+# ------------------------------------------------------------------ bias gradient (R17)
+def expected_bias_int(oracle_mod, dYall, K, out_dt):
+    """fl32(S_b * fl32(1/K)) (RNE to bf16 for a bf16 output) for integer dY: S_b is exact."""
+    S = oracle_mod.sfb_bias_sum(dYall[None])
+    e = S.astype(np.float32) * np.float32(1.0 / K)
+    if out_dt == "f32":
+        return e
+    return oracle_mod.bf16_bits_to_f64(oracle_mod.cast_bf16_bits(e)).astype(np.float32)
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 32, 8), (136, 264, 40), (4096, 1000, 256), (256, 512, 5),
+                                   (3, 5, 6), (130, 257, 10), (64, 32000, 256), (8, 8, 2048)])
+@pytest.mark.parametrize("out_dt", ["f32", "bf16"])
+def test_bias_grad_bit_exact(tag, comm1, oracle_mod, M, N, K, out_dt):
+    X = synth.draw("int3", K, M, synth.rng(60, M, N, 0))
+    dY = synth.draw("int3", K, N, synth.rng(60, M, N, 1))
+    plan = tag.SfbPlan(comm1, M, N, K, "bf16", "bf16", out_dt)
+    dW = torch.empty((M, N), dtype=TORCH[out_dt], device="cuda")
+    db = torch.full((N,), float("nan"), dtype=TORCH[out_dt], device="cuda")
+    Xd, dYd = to_dev(X, "bf16"), to_dev(dY, "bf16")
+    plan.sync(Xd, dYd, dW)
+    plan.bias_grad(db)
+    torch.cuda.synchronize()
+    plan.close()
+    got = db.float().cpu().numpy()
+    want = expected_bias_int(oracle_mod, dY, K, out_dt)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_bias_grad_random_fp32_wire_and_cast(tag, comm1, oracle_mod):
+    """fp32 wire (toy) and the fp32 -> bf16 cast path read the right dY_all; <= 1e-5 vs the oracle
+    on the operand values the GPU used."""
+    rs = np.random.default_rng(61)
+    for in_dt, wire_dt, M, N, K in (("f32", "f32", 64, 32, 8), ("f32", "bf16", 520, 1000, 64)):
+        X = rs.standard_normal((K, M)).astype(np.float32)
+        dY = rs.standard_normal((K, N)).astype(np.float32)
+        plan = tag.SfbPlan(comm1, M, N, K, in_dt, wire_dt, "f32")
+        dW = torch.empty((M, N), device="cuda")
+        db = torch.empty((N,), device="cuda")
+        plan.sync(to_dev(X, in_dt), to_dev(dY, in_dt), dW)
+        plan.bias_grad(db)
+        torch.cuda.synchronize()
+        plan.close()
+        want = oracle_mod.sfb_bias(exact_values(dY, wire_dt)[None])
+        assert rel_fro(db.cpu().numpy(), want) <= 1e-5
+
+
+def test_group_bias_grad_equals_per_plan(tag, comm1):
+    rs = np.random.default_rng(62)
+    layers = [(4096, 1000, 32), (1024, 4096, 32), (512, 2048, 32)]
+    plans, Xs, dYs, dWs = [], [], [], []
+    for M, N, K in layers:
+        plans.append(tag.SfbPlan(comm1, M, N, K))
+        Xs.append(torch.from_numpy(rs.standard_normal((K, M))).to(torch.bfloat16).cuda())
+        dYs.append(torch.from_numpy(rs.standard_normal((K, N))).to(torch.bfloat16).cuda())
+        dWs.append(torch.empty((M, N), device="cuda"))
+    g = tag.SfbGroup(plans)
+    g.sync(Xs, dYs, dWs)
+    dbs = [torch.empty((p.N,), device="cuda") for p in plans]
+    g.bias_grad(dbs)
+    for p, X, dY, dW, db in zip(plans, Xs, dYs, dWs, dbs):
+        p.sync(X, dY, dW)
+        one = torch.empty_like(db)
+        p.bias_grad(one)
+        torch.cuda.synchronize()
+        assert torch.equal(one, db)
+    g.close()
+    for p in plans:
+        p.close()
+
+
+def test_bias_grad_before_sync_is_an_error(tag, comm1):
+    plan = tag.SfbPlan(comm1, 64, 32, 8)
+    with pytest.raises(tag.TagError) as e:
+        plan.bias_grad(torch.empty((32,), device="cuda"))
+    assert e.value.status == tag.ERR_INVALID_ARG
+    plan.close()
