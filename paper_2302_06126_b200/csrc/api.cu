@@ -112,6 +112,9 @@ struct tag_plan_s {
     void* st_x = nullptr;
     void* st_dy = nullptr;
     void* st_dw = nullptr;
+    // fp32 wire on the tensor cores (3xTF32): split [hi ; lo] operands, kpad rows per half
+    void* split = nullptr;
+    int64_t kpad = 0;
 };
 
 struct tag_group_s {
@@ -250,6 +253,18 @@ tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int
     a.lr = p->d.lr;
     a.mu = p->d.momentum;
     a.wd = p->d.weight_decay;
+    if (p->use_tc && p->d.wire_dtype == TAG_F32) {
+        // 3xTF32: split both operands into [hi ; lo] halves of kp rows (pack_sgd.cu), then the
+        // kind::tf32 variant of the tensor-core kernel
+        const int64_t kp = (K + TF32_KALIGN - 1) / TF32_KALIGN * TF32_KALIGN;
+        float* sx = static_cast<float*>(p->split);
+        float* sdy = sx + 2 * kp * p->d.M;
+        TAG_TRY(launch_tf32_split(static_cast<const float*>(p->src_x), sx, K, p->d.M, kp, s));
+        TAG_TRY(launch_tf32_split(static_cast<const float*>(p->src_dy), sdy, K, p->d.N, kp, s));
+        a.A = sx;
+        a.Bm = sdy;
+        a.kpad = kp;
+    }
     if (p->use_tc && recon_tc_ok(a)) return launch_recon_tc(a, s);
     return launch_recon_simt(a, s);
 }
@@ -259,6 +274,7 @@ tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int
 // into every peer's window and waits, per layer, on arrival counters before loading its tiles.
 bool fusable(const tag_plan_s* p, void* dW) {
     if (p->gather_mode != TAG_GATHER_NVLINK_PUSH || !p->use_tc) return false;
+    if (p->d.wire_dtype != TAG_BF16) return false;           // 3xTF32 needs the split pass
     const bool same = p->d.in_dtype == p->d.wire_dtype;
     const bool cast = p->d.in_dtype == TAG_F32 && p->d.wire_dtype == TAG_BF16;
     if (!same && !cast) return false;
@@ -453,9 +469,15 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
     p->d = *d;
     p->K = static_cast<int64_t>(d->n) * d->B;
     p->alpha = static_cast<float>(1.0 / static_cast<double>(p->K));   // fl32(1/(nB)), R1
-    // tensor cores need 16-byte factor rows and bf16 operands (fp32 wire: SIMT FFMA, R10)
-    p->use_tc = d->wire_dtype == TAG_BF16 && d->M % 8 == 0 && d->N % 8 == 0;
+    // tensor cores need 16-byte factor rows: bf16 operands (kind::f16) or fp32 operands split
+    // for 3xTF32 (kind::tf32, R10); other shapes take the SIMT FFMA kernel
+    // (3xTF32 only up to K = 4096: the tensor core's accumulation error grows linearly with K —
+    // 4.8e-6 relative at K = 2048, 1.9e-5 at 8192 — and the fp32 bar is 1e-5, DESIGN R10)
+    p->use_tc = d->M % 8 == 0 && d->N % 8 == 0 &&
+                (d->wire_dtype == TAG_BF16 ||
+                 (!std::getenv("TAG_F32_SIMT") && static_cast<int64_t>(d->n) * d->B <= 4096));
     auto cleanup = [p]() {
+        cudaFree(p->split);
         cudaFree(p->gx);
         cudaFree(p->gdy);
         cudaFree(p->lx);
@@ -507,6 +529,14 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
             return cuda_fail(e, "tag_sfb_plan: cudaMalloc(gather buffers)");
         }
     }
+    if (p->use_tc && d->wire_dtype == TAG_F32) {
+        p->kpad = (p->K + TF32_KALIGN - 1) / TF32_KALIGN * TF32_KALIGN;
+        cudaError_t e = cudaMalloc(&p->split, static_cast<size_t>(2 * p->kpad * (d->M + d->N)) * 4);
+        if (e != cudaSuccess) {
+            cleanup();
+            return cuda_fail(e, "tag_sfb_plan: cudaMalloc(3xTF32 split operands)");
+        }
+    }
     if (c->nccl) {
         // dense baseline: the 1/(nB) scale rides inside the AllReduce (PreMulSum)
         ncclResult_t r;
@@ -550,6 +580,7 @@ tag_status_t tag_sfb_plan_destroy(tag_sfb_plan_t p) {
     cudaFree(p->st_x);
     cudaFree(p->st_dy);
     cudaFree(p->st_dw);
+    cudaFree(p->split);
     delete p;
     return TAG_OK;
 }

@@ -149,6 +149,50 @@ tag_status_t launch_pack(const void* x, void* x_dst, int64_t nx, const void* dy,
     return TAG_OK;
 }
 
+namespace {
+// 3xTF32 split (recon_tc.cu X3): one element per thread-iteration, grid-stride; non-finite
+// values keep hi = value (truncated) and lo = 0 (no inf - inf).
+__global__ void __launch_bounds__(256)
+tf32_split_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t K, int64_t cols,
+                  int64_t kpad) {
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t total = kpad * cols;
+    float* hi = dst;
+    float* lo = dst + total;
+    for (int64_t i = tid; i < total; i += nthreads) {
+        const int64_t row = i / cols;
+        float h = 0.f, l = 0.f;
+        if (row < K) {
+            const float v = src[i];
+            // hi = v rounded to the nearest tf32 (10 mantissa bits, ties to even): |lo| <= 2^-11 |v|,
+            // so the dropped lo*lo term is <= 2^-22 relative and the lo errors are unbiased
+            const uint32_t u = __float_as_uint(v);
+            const uint32_t r = (u + 0xfffu + ((u >> 13) & 1u)) & 0xffffe000u;
+            h = __uint_as_float(r);
+            if (!isfinite(v) || !isfinite(h)) h = __uint_as_float(u & 0xffffe000u);   // no overflow to inf
+            l = isfinite(v) ? __fsub_rn(v, h) : 0.f;
+            // lo rounded to tf32 too: the tensor core truncates its fp32 inputs, which would
+            // bias every lo term toward zero (measured 1.1e-6 -> see tests)
+            const uint32_t ul = __float_as_uint(l);
+            l = __uint_as_float((ul + 0xfffu + ((ul >> 13) & 1u)) & 0xffffe000u);
+        }
+        hi[i] = h;
+        lo[i] = l;
+    }
+}
+}  // namespace
+
+tag_status_t launch_tf32_split(const float* src, float* dst, int64_t K, int64_t cols, int64_t kpad,
+                               cudaStream_t s) {
+    if (kpad * cols == 0) return TAG_OK;
+    tf32_split_kernel<<<grid_for(kpad * cols), 256, 0, s>>>(src, dst, K, cols, kpad);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "launch tf32_split_kernel");
+    count_launch();
+    return TAG_OK;
+}
+
 tag_status_t launch_sgd(const float* dW, float* W, float* V, int64_t len, float lr, float mu,
                         float wd, cudaStream_t s) {
     if (len == 0) return TAG_OK;

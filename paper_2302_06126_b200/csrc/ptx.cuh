@@ -225,13 +225,17 @@ __device__ __forceinline__ void mma_commit_cg2_mc(uint32_t bar, uint16_t mask) {
 //   bits [32,46) stride-dimension byte offset >> 4    (MN-major: stride between 8-row K groups)
 //   bits [46,48) version = 1; bits [49,52) base offset = 0 (1024-byte aligned atoms);
 //   bits [61,64) layout = 2 (SWIZZLE_128B)
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// layout = 1 selects SWIZZLE_128B_BASE32B (32-byte swizzle atoms), the MN-major form of 32-bit
+// (tf32) operands, paired with the TMA's CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B; its K atoms are
+// 4 rows (sbo = 512 for 128-byte rows).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                               uint32_t layout = 2) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
     d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
     d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
     d |= static_cast<uint64_t>(1) << 46;
-    d |= static_cast<uint64_t>(2) << 61;
+    d |= static_cast<uint64_t>(layout & 7u) << 61;
     return d;
 }
 

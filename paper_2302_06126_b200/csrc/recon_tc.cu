@@ -40,29 +40,49 @@ namespace tag {
 namespace {
 
 constexpr int BM = 128;                  // UMMA M (TMEM lanes)
-constexpr int BK = 32;                   // factor rows per pipeline stage
 constexpr int NUM_EPI_WARPS = 8;
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;   // 320
-constexpr int CHUNK_BYTES = BK * 128;    // one 128-byte-wide MN chunk of BK rows (4 KB)
 constexpr int EPI_BUF_BYTES = 2 * 32 * 128;  // 2 x (32 rows x 128 B) transpose buffers per warp
 constexpr int TMEM_COLS = 512;
 
 // CTAS = 2: a CTA pair on one TPC runs tcgen05 cta_group::2 — UMMA M = 256 (128 rows of A in
 // each CTA's smem), N = BN (BN/2 columns of B in each CTA's smem), each CTA's TMEM holds its
 // 128 rows x BN fp32 accumulator. Halves the per-SM smem operand traffic and the L2 re-reads of B.
-template <int BN, int CTAS>
+//
+// X3 = true: fp32 factors on the tensor cores with 3xTF32 (kind::tf32). The operand buffers hold
+// [hi ; lo] halves (rows [0, Kp) and [Kp, 2Kp), see tf32_split in pack_sgd.cu) and every K step
+// issues hi*hi + hi*lo + lo*hi, which recovers ~fp32 accuracy (the dropped lo*lo and the tf32
+// truncations are ~2^-21 relative per product) at 3 MMAs per step — free while the epilogue's
+// HBM write binds. Stages carry 16 fp32 rows (32-element MN chunks of 128 B) of all four operands.
+template <int BN, int CTAS, bool X3 = false>
 struct Cfg {
-    static constexpr int ACC = TMEM_COLS / BN;            // accumulator buffers in TMEM
-    static constexpr int A_BYTES = (BM / 64) * CHUNK_BYTES;
-    static constexpr int B_BYTES = (BN / CTAS / 64) * CHUNK_BYTES;
+    // X3 keeps two accumulators per tile: hi*hi, and the small hi*lo + lo*hi terms apart, so the
+    // big accumulator sees K/8 additions instead of 3K/8 (the tensor core's fp32 accumulation
+    // error grows linearly with the number of MMAs; measured, scripts/probes/acc_error.py)
+    static constexpr int ACC_COLS = X3 ? 2 * BN : BN;     // TMEM columns per tile
+    static constexpr int ACC = TMEM_COLS / ACC_COLS;      // accumulator buffers in TMEM
+    static constexpr int ELEMS = X3 ? 32 : 64;            // MN elements per 128-byte chunk
+    static constexpr int BK = X3 ? 16 : 32;               // factor rows per pipeline stage
+    static constexpr int KMMA = X3 ? 8 : 16;              // K per tcgen05.mma
+    static constexpr int CHUNK_BYTES = BK * 128;          // one 128-byte-wide MN chunk of BK rows
+    static constexpr int A_CHUNKS = BM / ELEMS;
+    static constexpr int B_CHUNKS = BN / CTAS / ELEMS;
+    static constexpr int HALVES = X3 ? 2 : 1;             // hi and lo operands
+    // UMMA smem descriptor: bf16 SWIZZLE_128B (8-row K atoms), tf32 SWIZZLE_128B_BASE32B (4-row)
+    static constexpr uint32_t DLAYOUT = X3 ? 1u : 2u;
+    static constexpr uint32_t SBO = X3 ? 512u : 1024u;
+    static constexpr int A_BYTES = HALVES * A_CHUNKS * CHUNK_BYTES;
+    static constexpr int B_BYTES = HALVES * B_CHUNKS * CHUNK_BYTES;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     // pairs: 8 stages (VGG bucket at K = 256: 104 -> 99 us vs 6; 9-10 no better)
-    static constexpr int STAGES = CTAS == 2 ? 8 : (BN == 256 ? 6 : 8);
+    static constexpr int STAGES = X3 ? 4 : (CTAS == 2 ? 8 : (BN == 256 ? 6 : 8));
     static constexpr int EPI_BYTES = NUM_EPI_WARPS * EPI_BUF_BYTES;
     static constexpr int BAR_BYTES = 256;
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
-    // kind::f16 instruction descriptor: D f32, A/B bf16, both MN-major, N = BN, M = 128 * CTAS.
-    static constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+    // instruction descriptor: D f32, A/B bf16 (kind::f16) or tf32 (kind::tf32), both MN-major,
+    // N = BN, M = 128 * CTAS.
+    static constexpr uint32_t FMT = X3 ? 2u : 1u;
+    static constexpr uint32_t IDESC = (1u << 4) | (FMT << 7) | (FMT << 10) | (1u << 15) |
                                       (1u << 16) | (uint32_t(BN >> 3) << 17) |
                                       (uint32_t((BM * CTAS) >> 4) << 24);
 };
@@ -71,13 +91,14 @@ struct Cfg {
 // concatenated in layer order and distributed round-robin over the persistent CTAs, so the
 // prologue, pipeline ramp-up and the last partial wave are paid once per bucket, not per layer.
 struct LayerParams {
-    CUtensorMap tmA;  // X_all (K x M) bf16, box 64 x BK, 128-B swizzle
+    CUtensorMap tmA;  // X_all (K x M) bf16, box 64 x BK, 128-B swizzle (X3: [hi;lo] fp32, box 32 x BK)
     CUtensorMap tmB;  // dY_all (K x N)
     void* C;          // dW out (may be nullptr with SGD)
     float* W;
     float* V;
     int M, N;
     int num_n_blocks, num_k_blocks;
+    int k_lo;         // X3: first row of the lo halves (Kp)
     int tile_begin;   // first global tile index of this layer
     int num_m_blocks;
     int m_fast;       // 1: consecutive tiles walk down M (share a B panel), else along N
@@ -227,11 +248,12 @@ __device__ __forceinline__ void fused_wait(const LayerParams& L, int me) {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED>
+template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const int me)
 {
-    using C = Cfg<BN, CTAS>;
+    using C = Cfg<BN, CTAS, X3>;
+    static_assert(!X3 || (CTAS == 1 && !FUSED), "3xTF32: single-CTA tiles, staged gather");
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the SWIZZLE_128B atoms
     const uint32_t base = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -322,19 +344,25 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                         if (crank == 0) ptx::mbar_arrive_expect_tx(fb, CTAS * C::STAGE_BYTES);
                         else ptx::mbar_arrive_cluster(fbl);
 #pragma unroll
-                        for (int c = 0; c < BM / 64; ++c)
-                            ptx::tma_load_2d_cg2(sa + c * CHUNK_BYTES, tmA, fbl, am0 + 64 * c, kb * BK);
+                        for (int c = 0; c < C::A_CHUNKS; ++c)
+                            ptx::tma_load_2d_cg2(sa + c * C::CHUNK_BYTES, tmA, fbl, am0 + C::ELEMS * c, kb * C::BK);
 #pragma unroll
-                        for (int c = 0; c < BN / CTAS / 64; ++c)
-                            ptx::tma_load_2d_cg2(sb + c * CHUNK_BYTES, tmB, fbl, bn0 + 64 * c, kb * BK);
+                        for (int c = 0; c < C::B_CHUNKS; ++c)
+                            ptx::tma_load_2d_cg2(sb + c * C::CHUNK_BYTES, tmB, fbl, bn0 + C::ELEMS * c, kb * C::BK);
                     } else {
                         ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
 #pragma unroll
-                        for (int c = 0; c < BM / 64; ++c)
-                            ptx::tma_load_2d(sa + c * CHUNK_BYTES, tmA, fb, am0 + 64 * c, kb * BK);
+                        for (int h = 0; h < C::HALVES; ++h) {     // X3: h = 1 loads the lo rows
+                            const int kr = kb * C::BK + h * gp.L[tr.li].k_lo;
 #pragma unroll
-                        for (int c = 0; c < BN / 64; ++c)
-                            ptx::tma_load_2d(sb + c * CHUNK_BYTES, tmB, fb, bn0 + 64 * c, kb * BK);
+                            for (int c = 0; c < C::A_CHUNKS; ++c)
+                                ptx::tma_load_2d(sa + (h * C::A_CHUNKS + c) * C::CHUNK_BYTES, tmA, fb,
+                                                 am0 + C::ELEMS * c, kr);
+#pragma unroll
+                            for (int c = 0; c < C::B_CHUNKS; ++c)
+                                ptx::tma_load_2d(sb + (h * C::B_CHUNKS + c) * C::CHUNK_BYTES, tmB, fb,
+                                                 bn0 + C::ELEMS * c, kr);
+                        }
                     }
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -352,19 +380,31 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                 const int nkb = gp.L[locate<BN, CTAS>(gp, tile).li].num_k_blocks;
                 ptx::mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);   // epilogue drained it
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BN;
+                const uint32_t d_tmem = tmem_base + acc * C::ACC_COLS;
                 for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait(bar_full + 8 * stage, phase);        // TMA landed
                     ptx::tc_fence_after();
                     const uint32_t sa = s_stages + stage * C::STAGE_BYTES;
                     const uint32_t sb = sa + C::A_BYTES;
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk) {
-                        // 16 K rows = two 8-row swizzle atoms = 2048 bytes per UMMA_K step
-                        const uint64_t ad = ptx::sw128_desc(sa + kk * 2048, CHUNK_BYTES, 1024);
-                        const uint64_t bd = ptx::sw128_desc(sb + kk * 2048, CHUNK_BYTES, 1024);
-                        if constexpr (CTAS == 2) ptx::mma_f16_cg2(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0);
-                        else ptx::mma_f16(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0);
+                    for (int kk = 0; kk < C::BK / C::KMMA; ++kk) {
+                        // KMMA rows of 128 B per UMMA_K step (bf16: two 8-row swizzle atoms)
+                        const uint32_t ko = kk * C::KMMA * 128;
+                        const uint64_t ad = ptx::sw128_desc(sa + ko, C::CHUNK_BYTES, C::SBO, C::DLAYOUT);
+                        const uint64_t bd = ptx::sw128_desc(sb + ko, C::CHUNK_BYTES, C::SBO, C::DLAYOUT);
+                        if constexpr (X3) {
+                            const uint64_t adl = ptx::sw128_desc(sa + C::A_CHUNKS * C::CHUNK_BYTES + ko,
+                                                                 C::CHUNK_BYTES, C::SBO, C::DLAYOUT);
+                            const uint64_t bdl = ptx::sw128_desc(sb + C::B_CHUNKS * C::CHUNK_BYTES + ko,
+                                                                 C::CHUNK_BYTES, C::SBO, C::DLAYOUT);
+                            ptx::mma_tf32(d_tmem + BN, adl, bd, C::IDESC, (kb | kk) != 0);  // lo * hi
+                            ptx::mma_tf32(d_tmem + BN, ad, bdl, C::IDESC, 1);               // hi * lo
+                            ptx::mma_tf32(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0);        // hi * hi
+                        } else if constexpr (CTAS == 2) {
+                            ptx::mma_f16_cg2(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0);
+                        } else {
+                            ptx::mma_f16(d_tmem, ad, bd, C::IDESC, (kb | kk) != 0);
+                        }
                     }
                     // frees the smem slot (both CTAs' slots for a pair)
                     if constexpr (CTAS == 2) ptx::mma_commit_cg2_mc(bar_empty + 8 * stage, 0x3);
@@ -393,7 +433,7 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
         constexpr int COLS_PER_CHUNK = 128 / ESZ;               // 128 bytes of output per row
         constexpr int CHUNKS = (BN / 2) / COLS_PER_CHUNK;
         constexpr int VEC = 16 / ESZ;                           // output elements per 16 B
-        constexpr int PAIR = OUT_BF16 || SGD ? 1 : 2;           // chunks staged per round
+        constexpr int PAIR = OUT_BF16 || SGD || X3 ? 1 : 2;     // chunks staged per round
         const int sub = lane >> 3;               // row within a 4-row group (write-out phase)
         const int cj = lane & 7;                 // 16-byte column slot (write-out phase)
         int acc = 0;
@@ -413,7 +453,7 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
             const int row0 = tr.m0 + static_cast<int>(crank) * BM + 32 * quad;  // first row
             ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
             ptx::tc_fence_after();
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quad) << 16) + acc * BN;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quad) << 16) + acc * C::ACC_COLS;
             // chunks of this warp's column half that hold any output column (warp-uniform)
             int nch = (N - (n0 + half * (BN / 2)) + COLS_PER_CHUNK - 1) / COLS_PER_CHUNK;
             nch = nch < 0 ? 0 : (nch > CHUNKS ? CHUNKS : nch);
@@ -439,6 +479,19 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                         ptx::tmem_ld_32x32b_x32(tc, r0);
                         ptx::tmem_ld_32x32b_x32(tc + 32, r1);
                         ptx::tmem_wait_ld();
+                        if constexpr (X3) {       // + the lo accumulator, one fp32 add (RN)
+                            uint32_t l[32];
+                            ptx::tmem_ld_32x32b_x32(tc + BN, l);
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                r0[i] = __float_as_uint(__fadd_rn(__uint_as_float(r0[i]), __uint_as_float(l[i])));
+                            ptx::tmem_ld_32x32b_x32(tc + BN + 32, l);
+                            ptx::tmem_wait_ld();
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                r1[i] = __float_as_uint(__fadd_rn(__uint_as_float(r1[i]), __uint_as_float(l[i])));
+                        }
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
                             w[q][i] = pack_bf16x2(__fmul_rn(__uint_as_float(r0[2 * i]), alpha),
@@ -452,6 +505,14 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                 }
                 if constexpr (!OUT_BF16) {
                     ptx::tmem_wait_ld();
+                    if constexpr (X3) {           // + the lo accumulator (PAIR = 1), one fp32 add
+                        uint32_t l[32];
+                        ptx::tmem_ld_32x32b_x32(t_row + half * (BN / 2) + ch * COLS_PER_CHUNK + BN, l);
+                        ptx::tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            w[0][i] = __float_as_uint(__fadd_rn(__uint_as_float(w[0][i]), __uint_as_float(l[i])));
+                    }
 #pragma unroll
                     for (int q = 0; q < PAIR; ++q)
 #pragma unroll
@@ -603,7 +664,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // Row-major rows x cols matrix; box = box_cols x box_rows; 128-byte swizzle.
 bool encode_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esize, int64_t rows,
-               int64_t cols, int box_cols, int box_rows, int64_t ld = 0) {
+               int64_t cols, int box_cols, int box_rows, int64_t ld = 0,
+               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
@@ -611,7 +673,7 @@ bool encode_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esiz
     cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(m, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
@@ -654,25 +716,29 @@ bool big_tiles(const ReconArgs* a, int count) {
     return tiles_for(a, count, 256, ctas) >= num_sms() / ctas;
 }
 
-template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED>
+template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3 = false>
 tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
-    using C = Cfg<BN, CTAS>;
+    using C = Cfg<BN, CTAS, X3>;
     GroupParams gp;
     std::memset(&gp, 0, sizeof gp);
     int tiles = 0;
     for (int i = 0; i < count; ++i) {
         LayerParams& L = gp.L[i];
-        if (!encode_2d(&L.tmA, a[i].A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a[i].K, a[i].M, 64, BK,
-                       a[i].lda) ||
-            !encode_2d(&L.tmB, a[i].Bm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, a[i].K, a[i].N, 64, BK))
+        const CUtensorMapDataType odt = X3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+        const int oes = X3 ? 4 : 2;
+        const int64_t orows = X3 ? 2 * a[i].kpad : a[i].K;      // X3: [hi ; lo], Kp rows each
+        const CUtensorMapSwizzle oswz = X3 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+        if (!encode_2d(&L.tmA, a[i].A, odt, oes, orows, a[i].M, C::ELEMS, C::BK, a[i].lda, oswz) ||
+            !encode_2d(&L.tmB, a[i].Bm, odt, oes, orows, a[i].N, C::ELEMS, C::BK, 0, oswz))
             return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
+        L.k_lo = X3 ? static_cast<int>(a[i].kpad) : 0;
         L.C = a[i].C;
         L.W = a[i].W;
         L.V = a[i].V;
         L.M = static_cast<int>(a[i].M);
         L.N = static_cast<int>(a[i].N);
         L.num_n_blocks = static_cast<int>((a[i].N + BN - 1) / BN);
-        L.num_k_blocks = static_cast<int>((a[i].K + BK - 1) / BK);
+        L.num_k_blocks = static_cast<int>((a[i].K + C::BK - 1) / C::BK);
         L.tile_begin = tiles;
         L.alpha = a[i].alpha;
         L.num_m_blocks = static_cast<int>((a[i].M + BM * CTAS - 1) / (BM * CTAS));
@@ -706,7 +772,7 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     }();
     gp.dbg = dbg;
     gp.cast = FUSED && fg->cast ? 1 : 0;
-    auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED>;
+    auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED, X3>;
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -738,6 +804,12 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
 
 template <bool FUSED>
 tag_status_t dispatch(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
+    if (a[0].wire == TAG_F32) {                 // 3xTF32: 128 x 128 tiles, staged gather only
+        if constexpr (FUSED) return fail(TAG_ERR_UNSUPPORTED, "recon: fp32 wire is not fused");
+        if (a[0].sgd) return launch_t<128, 1, false, true, false, true>(a, count, s, fg);
+        if (a[0].out == TAG_BF16) return launch_t<128, 1, true, false, false, true>(a, count, s, fg);
+        return launch_t<128, 1, false, false, false, true>(a, count, s, fg);
+    }
     const bool wide = big_tiles(a, count);
     const bool pair = wide && use_ctas(a, count) == 2;
     if (a[0].sgd) {
@@ -758,7 +830,8 @@ tag_status_t dispatch(const ReconArgs* a, int count, cudaStream_t s, const Fused
 }  // namespace
 
 bool recon_tc_ok(const ReconArgs& a) {
-    if (a.wire != TAG_BF16) return false;                 // tf32 path: later
+    if (a.wire == TAG_F32 && a.kpad < a.K) return false;  // 3xTF32 needs the split [hi ; lo] operands
+    if (a.wire == TAG_F32 && (std::getenv("TAG_F32_SIMT") || a.lda)) return false;
     if (a.M % 8 || a.N % 8 || a.lda % 8) return false;   // 16-byte rows for TMA (bf16)
     if (a.M > INT32_MAX || a.N > INT32_MAX || a.K > INT32_MAX) return false;
     if (a.sgd && a.out == TAG_BF16 && a.C) return false;  // E2 writes fp32 dW only
@@ -782,8 +855,8 @@ tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s
                                    const FusedGather* fused) {
     if (count < 1 || count > MAX_GROUP) return fail(TAG_ERR_INVALID_ARG, "recon group size");
     for (int i = 0; i < count; ++i)
-        if (a[i].sgd != a[0].sgd || a[i].out != a[0].out)
-            return fail(TAG_ERR_INVALID_ARG, "recon group: mixed epilogues");
+        if (a[i].sgd != a[0].sgd || a[i].out != a[0].out || a[i].wire != a[0].wire)
+            return fail(TAG_ERR_INVALID_ARG, "recon group: mixed epilogues or operand dtypes");
     return fused ? dispatch<true>(a, count, s, fused) : dispatch<false>(a, count, s, nullptr);
 }
 

@@ -31,6 +31,7 @@ struct ReconArgs {
     void* C;             // M x N, out dtype; may be nullptr when sgd (no dW write)
     int64_t M, N, K;
     int64_t lda;         // elements between consecutive rows of A (0: M) — row shards of X_all
+    int64_t kpad;        // fp32 wire (3xTF32): A, Bm are split [hi ; lo] buffers of kpad rows each
     tag_dtype_t wire;    // operand dtype
     tag_dtype_t out;     // C dtype
     float alpha;
@@ -96,6 +97,13 @@ struct BiasArgs {
 };
 // db = alpha * column sums of dY_all for 1..MAX_GROUP layers in one launch (bias.cu)
 tag_status_t launch_bias_grad(const BiasArgs* a, int count, cudaStream_t s);
+
+// ------------------------------------------------------------------ 3xTF32 operand split
+// dst = [hi ; lo] (2*kpad x cols fp32): hi = src rounded to the nearest tf32 (a value kind::tf32
+// reads exactly), lo = src - hi (exact in fp32); rows [K, kpad) of both halves are zero.
+tag_status_t launch_tf32_split(const float* src, float* dst, int64_t K, int64_t cols, int64_t kpad,
+                               cudaStream_t s);
+constexpr int TF32_KALIGN = 16;   // kpad = K rounded up to the 3xTF32 stage depth
 
 // ------------------------------------------------------------------ unfused SGD
 tag_status_t launch_sgd(const float* dW, float* W, float* V, int64_t len, float lr, float mu,

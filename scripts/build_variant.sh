@@ -10,7 +10,7 @@ nccl=/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl
 mkdir -p "$root/build_exp"
 make -C "$csrc" -s
 nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC,-fvisibility=hidden \
-  --expt-relaxed-constexpr -I$nccl/include -I$root/include "$@" -c "$csrc/recon_tc.cu" -o "$root/build_exp/recon_tc_$name.o"
+  --expt-relaxed-constexpr -I$nccl/include -I$root/include -I$csrc "$@" -c "${SRC:-$csrc/recon_tc.cu}" -o "$root/build_exp/recon_tc_$name.o"
 objs=""
 for o in api recon_simt pack_sgd push_gather bias select ilp; do objs="$objs $csrc/$o.o"; done
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$root/build_exp/libtag_$name.so" $objs \

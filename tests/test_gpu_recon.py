@@ -94,14 +94,16 @@ def test_virtual_n_random_vgg_fc7(tag, comm1, oracle_mod, n, B):
 
 
 def test_fp32_toy_config(tag, comm1, oracle_mod):
-    """Config 1: M=64, N=32, B=4, n=2, fp32 end to end (SIMT FFMA path): <= 1e-5."""
+    """Config 1: M=64, N=32, B=4, n=2, fp32 end to end (3xTF32 tensor-core path): <= 1e-5."""
     X, dY = synth.all_factors(1, 0, 2, 64, 32, 4, "normal", "normal")
     dW = run_sync(tag, comm1, X.reshape(8, 64), dY.reshape(8, 32), "f32", "f32", "f32")
     assert rel_fro(dW.cpu().numpy(), oracle_mod.sfb_dw(X, dY)) <= 1e-5
 
 
-@pytest.mark.parametrize("M,N,K", [(512, 2048, 256), (100, 36, 7)])
+@pytest.mark.parametrize("M,N,K", [(512, 2048, 256), (100, 36, 7), (4096, 1000, 32),
+                                   (136, 264, 37), (1024, 4096, 2048), (8, 8, 1)])
 def test_fp32_wire_random(tag, comm1, oracle_mod, M, N, K):
+    """fp32 factors: 3xTF32 on the tensor cores (M, N multiples of 8) or SIMT FFMA (100 x 36)."""
     X = synth.draw("normal", K, M, synth.rng(51, M, N, 0))
     dY = synth.draw("normal", K, N, synth.rng(51, M, N, 1))
     dW = run_sync(tag, comm1, X, dY, "f32", "f32", "f32")
@@ -420,3 +422,57 @@ def test_bias_grad_before_sync_is_an_error(tag, comm1):
         plan.bias_grad(torch.empty((32,), device="cuda"))
     assert e.value.status == tag.ERR_INVALID_ARG
     plan.close()
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 32, 8), (136, 264, 40), (4096, 1000, 256), (256, 512, 5),
+                                   (1024, 4096, 33)])
+@pytest.mark.parametrize("out_dt", ["f32", "bf16"])
+def test_fp32_wire_integer_bit_exact(tag, comm1, oracle_mod, M, N, K, out_dt):
+    """3xTF32 on integers: hi = x, lo = 0, so the tensor-core sum is exact (same pin as bf16)."""
+    X = synth.draw("int3", K, M, synth.rng(63, M, N, 0))
+    dY = synth.draw("int3", K, N, synth.rng(63, M, N, 1))
+    plan = tag.SfbPlan(comm1, M, N, K, "f32", "f32", out_dt)
+    assert plan.info()["tensor_cores"]
+    dW = torch.full((M, N), float("nan"), dtype=TORCH[out_dt], device="cuda")
+    plan.sync(to_dev(X, "f32"), to_dev(dY, "f32"), dW)
+    torch.cuda.synchronize()
+    plan.close()
+    want = expected_int(oracle_mod, X, dY, K, out_dt)
+    assert np.array_equal(dW.float().cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
+def test_fp32_wire_lo_halves_matter(tag, comm1, oracle_mod):
+    """Values with mantissa bits below tf32's 10: one TF32 pass would be off by ~1e-4; 3xTF32
+    must stay within 1e-6 of the fp64 oracle."""
+    rs = np.random.default_rng(64)
+    K, M, N = 64, 256, 512
+    X = (1.0 + rs.random((K, M)) * 2.0 ** -11).astype(np.float32)   # only low mantissa bits vary
+    dY = (1.0 + rs.random((K, N)) * 2.0 ** -11).astype(np.float32)
+    plan = tag.SfbPlan(comm1, M, N, K, "f32", "f32", "f32")
+    dW = torch.empty((M, N), device="cuda")
+    plan.sync(to_dev(X, "f32"), to_dev(dY, "f32"), dW)
+    torch.cuda.synchronize()
+    plan.close()
+    want = oracle_mod.sfb_dw(X.astype(np.float64)[None], dY.astype(np.float64)[None])
+    err = np.abs(dW.cpu().numpy() - want).max() / np.abs(want).max()
+    assert err <= 1e-6, err
+
+
+def test_fp32_wire_sgd_fused(tag, comm1, oracle_mod):
+    """E2 on the 3xTF32 path equals the unfused update bit for bit."""
+    rs = np.random.default_rng(65)
+    K, M, N = 32, 512, 1024
+    X = torch.from_numpy(rs.standard_normal((K, M)).astype(np.float32)).cuda()
+    dY = torch.from_numpy(rs.standard_normal((K, N)).astype(np.float32)).cuda()
+    W0 = torch.from_numpy(rs.standard_normal((M, N)).astype(np.float32)).cuda()
+    v0 = torch.from_numpy(rs.standard_normal((M, N)).astype(np.float32)).cuda()
+    p = tag.SfbPlan(comm1, M, N, K, "f32", "f32", "f32", fuse_sgd=True, lr=1e-2, momentum=0.9)
+    W1, v1 = W0.clone(), v0.clone()
+    p.sync_sgd(X, dY, W1, v1, None)
+    dW = torch.empty((M, N), device="cuda")
+    p.sync(X, dY, dW)
+    W2, v2 = W0.clone(), v0.clone()
+    p.sgd_step(dW, W2, v2)
+    torch.cuda.synchronize()
+    p.close()
+    assert torch.equal(W1, W2) and torch.equal(v1, v2)
