@@ -249,7 +249,8 @@ def main():
     if n > 1 and os.path.exists(prof_path):
         prof = json.load(open(prof_path))
         choices_prof = tag.select_profiled(sel_layers, n, prof["gather"], prof["allreduce"],
-                                           int(peaks.get("bf16_tflops_sustained", 1400) * 1e12))
+                                           int(peaks.get("bf16_tflops_sustained", 1400) * 1e12),
+                                           prof.get("ps"))
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     flush_rd = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -416,7 +417,7 @@ def main():
             "recon_tensor_frac": round(flops / (t_rec * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
             "allgather_busbw_GBps": round(ag / ((t_sync - t_rec) * 1e-3) / 1e9, 1) if n > 1 else None,
             "selector": {0: "allreduce", 1: "sfb", 2: "none"}[choices[i]],
-            "selector_profiled": ({0: "allreduce", 1: "sfb", 2: "none"}[choices_prof[i]]
+            "selector_profiled": ({0: "allreduce", 1: "sfb", 2: "none", 3: "ps"}[choices_prof[i]]
                                   if choices_prof else None),
             "gather": l["plan"].info()["gather"] + ("+multicast" if l["plan"].info()["multicast"] else "")}
     if group is not None and n > 1 and staged_g_ms:
@@ -440,9 +441,22 @@ def main():
                 torch.cuda.synchronize()
                 t.append(e0.elapsed_time(e1))
             td = tdist.max_over_ranks(statistics.median(t))
+            # Replicate-with-PS: the same local gradient, reduced to a round-robin PS
+            # (root = layer index mod n) and broadcast back
+            t = []
+            for _ in range(max(3, min(args.steps, 10))):
+                e0, e1 = start_events(2)
+                l["plan"].local_grad(l["X"], l["dY"], l["dW"], stream)
+                l["plan"].ps_sync(l["dW"], i % n, stream)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                t.append(e0.elapsed_time(e1))
+            tp = tdist.max_over_ranks(statistics.median(t))
             per_layer[L.name]["dense_us"] = round(td * 1e3, 2)
+            per_layer[L.name]["ps_us"] = round(tp * 1e3, 2)
             per_layer[L.name]["sfb_speedup_vs_dense"] = round(td / (per_layer[L.name]["sync_us"] / 1e3), 2)
-            per_layer[L.name]["measured_winner"] = "sfb" if per_layer[L.name]["sync_us"] < td * 1e3 else "allreduce"
+            per_layer[L.name]["measured_winner"] = min(
+                [(per_layer[L.name]["sync_us"], "sfb"), (td * 1e3, "allreduce"), (tp * 1e3, "ps")])[1]
 
     # ---------------------------------------------------------------- sharded variant (n > 1)
     # every rank still receives all factors but reconstructs only its

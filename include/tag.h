@@ -62,9 +62,15 @@ typedef enum {
 
 typedef enum { TAG_F32 = 0, TAG_BF16 = 1 } tag_dtype_t;
 
-/* Per-layer synchronisation choice: Replicate-with-AllReduce, or SFB
- * ("Duplicate" of the gradient op, P:363-365 / P:523-524); NONE when n = 1. */
-typedef enum { TAG_SYNC_ALLREDUCE = 0, TAG_SYNC_SFB = 1, TAG_SYNC_NONE = 2 } tag_choice_t;
+/* Per-layer synchronisation choice: Replicate-with-AllReduce, SFB
+ * ("Duplicate" of the gradient op, P:363-365 / P:523-524), Replicate-with-PS (only
+ * from the profiled selector when a PS curve is given); NONE when n = 1. */
+typedef enum {
+    TAG_SYNC_ALLREDUCE = 0,
+    TAG_SYNC_SFB = 1,
+    TAG_SYNC_NONE = 2,
+    TAG_SYNC_PS = 3
+} tag_choice_t;
 
 /* Readings of the SFB communication term (DESIGN R2): north_star's gathered bytes n*S (default),
  * the paper ILP's D(D-1)*S broadcast term, or the physical all-gather wire (n-1)*S. */
@@ -251,6 +257,14 @@ tag_status_t tag_local_grad(tag_sfb_plan_t plan, const void* X, const void* dY, 
  * applies the scale inside the collective (P:566 ring AllReduce). dW: M x N out_dtype.
  * n = 1: dW <- dW / B. */
 tag_status_t tag_dense_allreduce(tag_sfb_plan_t plan, void* dW, tag_stream_t stream);
+/* COLLECTIVE. "Replicate with PS": the parameter server `root` aggregates the local
+ * gradients (AddN, with the 1/(nB) scale as PreMulSum: ncclReduce) and sends the result back to
+ * every replica (ncclBroadcast). In place, like tag_dense_allreduce: dW (M x N out_dtype) holds
+ * this rank's unscaled local gradient on entry and (1/(nB)) * sum_ranks dW on exit, bitwise
+ * identical on every rank. The paper picks the PS round-robin over the device group
+ * (S:367): pass root = layer index mod n. n = 1: dW <- dW / B. Errors:
+ * TAG_ERR_INVALID_ARG (root outside [0, n), NULL / misaligned dW). */
+tag_status_t tag_ps_sync(tag_sfb_plan_t plan, void* dW, int root, tag_stream_t stream);
 /* Unfused optimizer step of the dense path (same arithmetic as the fused epilogue):
  * g = dW + wd*W; v <- momentum*v + g; W <- W - lr*v. dW fp32 (out_dtype must be F32). */
 tag_status_t tag_sgd_step(tag_sfb_plan_t plan, const float* dW, float* W, float* v,
@@ -292,7 +306,9 @@ tag_status_t tag_sfb_select(const tag_layer_t* layers, int num_layers, const tag
  * last segment outside them, evaluated in integer ns with floor rounding and clamped
  * at 0. Decision per layer (S = B(M+N)e_w, G = M N e_g):
  *   SFB iff gather((n-1) S) + floor((n-1) 2MNB 1e9 / F) < allreduce(G)   [F = 0: no compute term]
- * ties keep AllReduce; n = 1 -> NONE. Exact integer arithmetic (bit-identical on every rank and
+ * ties keep AllReduce; n = 1 -> NONE. With a PS curve (ps.count >= 2; count 0 = no PS option,
+ * "Replicate with PS"), PS is chosen iff ps(G) is strictly below both other costs
+ * (ties: AllReduce, then SFB). Exact integer arithmetic (bit-identical on every rank and
  * to oracle/selector.py). Limits (TAG_ERR_INVALID_ARG beyond): n <= 65536, M, N, B <= 2^24,
  * curve ns <= 2^40, bytes <= 2^62. */
 typedef struct {
@@ -305,6 +321,7 @@ typedef struct {
     tag_curve_t gather;      /* x = bytes each rank receives: (n-1) * B(M+N) e_w */
     tag_curve_t allreduce;   /* x = gradient bytes M N e_g */
     uint64_t tensor_flops;   /* F; 0 drops the compute term */
+    tag_curve_t ps;          /* x = gradient bytes M N e_g (tag_ps_sync); count 0: no PS option */
 } tag_profiled_topology_t;
 tag_status_t tag_sfb_select_profiled(const tag_layer_t* layers, int num_layers,
                                      const tag_profiled_topology_t* topo, tag_choice_t* out);

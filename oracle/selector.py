@@ -33,6 +33,7 @@ RULE_WIRE = 2
 CHOICE_ALLREDUCE = 0
 CHOICE_SFB = 1
 CHOICE_NONE = 2
+CHOICE_PS = 3            # Replicate with PS, profiled selector only
 
 
 def sfb_elements_fig5(H1, H2, B):
@@ -137,8 +138,10 @@ def curve_ns(points, x):
     return max(t, 0)
 
 
-def select_profiled(layer, n, gather_pts, allreduce_pts, F=0):
-    """SFB iff gather((n-1) S) + floor((n-1) 2MNB 1e9 / F) < allreduce(G); ties -> AllReduce."""
+def select_profiled(layer, n, gather_pts, allreduce_pts, F=0, ps_pts=None):
+    """SFB iff gather((n-1) S) + floor((n-1) 2MNB 1e9 / F) < allreduce(G); ties -> AllReduce.
+    With a PS curve ("Replicate with PS"): PS iff ps(G) is strictly below both
+    (ties: AllReduce, then SFB)."""
     if n <= 1:
         return CHOICE_NONE
     M, N, B, e_w, e_g = layer["M"], layer["N"], layer["B"], layer["e_w"], layer["e_g"]
@@ -147,7 +150,10 @@ def select_profiled(layer, n, gather_pts, allreduce_pts, F=0):
     t_sfb = curve_ns(gather_pts, (n - 1) * S)
     if F:
         t_sfb += ((n - 1) * 2 * M * N * B * 10 ** 9) // F
-    return CHOICE_SFB if t_sfb < curve_ns(allreduce_pts, G) else CHOICE_ALLREDUCE
+    costs = [(curve_ns(allreduce_pts, G), 0, CHOICE_ALLREDUCE), (t_sfb, 1, CHOICE_SFB)]
+    if ps_pts:
+        costs.append((curve_ns(ps_pts, G), 2, CHOICE_PS))
+    return min(costs)[2]
 
 
 # ---------------------------------------------------------------------------------------------

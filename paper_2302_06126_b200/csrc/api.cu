@@ -758,6 +758,25 @@ tag_status_t tag_dense_allreduce(tag_sfb_plan_t p, void* dW, tag_stream_t stream
     return TAG_OK;
 }
 
+tag_status_t tag_ps_sync(tag_sfb_plan_t p, void* dW, int root, tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_ps_sync: NULL plan");
+    TAG_TRY(check_ptrs("tag_ps_sync", {dW}));
+    if (root < 0 || root >= p->comm->nranks)
+        return fail(TAG_ERR_INVALID_ARG, "tag_ps_sync: root must be a rank of the comm");
+    if (!p->comm->nccl) return tag_dense_allreduce(p, dW, stream);     // n = 1: dW / B
+    TAG_TRY(set_device(p->comm));
+    TAG_TRY(check_async(p->comm));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t len = static_cast<size_t>(p->d.M * p->d.N);
+    const ncclDataType_t t = nccl_type(p->d.out_dtype);
+    // AddN on the PS (PreMulSum applies 1/(nB) inside the reduction), then the PS sends it back
+    ncclResult_t r = ncclReduce(dW, dW, len, t, p->premul, root, p->comm->nccl, s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclReduce");
+    r = ncclBroadcast(dW, dW, len, t, root, p->comm->nccl, s);
+    if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast");
+    return TAG_OK;
+}
+
 tag_status_t tag_sgd_step(tag_sfb_plan_t p, const float* dW, float* W, float* v,
                           tag_stream_t stream) {
     if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sgd_step: NULL plan");

@@ -147,6 +147,9 @@ extern "C" tag_status_t tag_sfb_select_profiled(const tag_layer_t* layers, int n
     if (!curve_ok(topo->gather) || !curve_ok(topo->allreduce))
         return fail(TAG_ERR_INVALID_ARG,
                     "tag_sfb_select_profiled: curves need >= 2 points with increasing bytes");
+    const bool has_ps = topo->ps.count != 0;
+    if (has_ps && !curve_ok(topo->ps))
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_select_profiled: bad PS curve");
     for (int i = 0; i < num_layers; ++i) {
         const tag_layer_t& L = layers[i];
         if (L.M < 1 || L.N < 1 || L.B < 1 || L.M > (1ll << 24) || L.N > (1ll << 24) ||
@@ -170,7 +173,12 @@ extern "C" tag_status_t tag_sfb_select_profiled(const tag_layer_t* layers, int n
         i128 t_sfb = curve_ns(topo->gather, (n - 1) * S);
         if (F > 0) t_sfb += floor_div((n - 1) * 2 * M * N * B * 1000000000, F);
         const i128 t_ar = curve_ns(topo->allreduce, G);
-        out[i] = t_sfb < t_ar ? TAG_SYNC_SFB : TAG_SYNC_ALLREDUCE;
+        // AllReduce unless strictly beaten; then SFB; then PS if strictly below the best so far
+        tag_choice_t c = TAG_SYNC_ALLREDUCE;
+        i128 best = t_ar;
+        if (t_sfb < best) { c = TAG_SYNC_SFB; best = t_sfb; }
+        if (has_ps && curve_ns(topo->ps, G) < best) c = TAG_SYNC_PS;
+        out[i] = c;
     }
     return TAG_OK;
 }

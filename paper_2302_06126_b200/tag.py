@@ -23,7 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 OK, ERR_INVALID_ARG, ERR_UNSUPPORTED, ERR_CUDA, ERR_NCCL, ERR_OOM, ERR_NOT_INITIALIZED, ERR_ASYNC = \
     range(8)
 F32, BF16 = 0, 1
-SYNC_ALLREDUCE, SYNC_SFB, SYNC_NONE = 0, 1, 2
+SYNC_ALLREDUCE, SYNC_SFB, SYNC_NONE, SYNC_PS = 0, 1, 2, 3
 RULE_NORTHSTAR, RULE_PAPER_ILP, RULE_WIRE = 0, 1, 2
 
 _TORCH_DT = {F32: torch.float32, BF16: torch.bfloat16}
@@ -58,7 +58,7 @@ class Curve(ctypes.Structure):
 
 class ProfiledTopology(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("gather", Curve), ("allreduce", Curve),
-                ("tensor_flops", ctypes.c_uint64)]
+                ("tensor_flops", ctypes.c_uint64), ("ps", Curve)]
 
 
 class IlpInstance(ctypes.Structure):
@@ -98,6 +98,7 @@ _SIGS = {
     "tag_sfb_sync_sharded": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_local_grad": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_dense_allreduce": ([_vp, _vp, _vp], _st),
+    "tag_ps_sync": ([_vp, _vp, _i, _vp], _st),
     "tag_sgd_step": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_select": ([_p(LayerDesc), _i, _p(Topology), _p(_i)], _st),
     "tag_sfb_select_profiled": ([_p(LayerDesc), _i, _p(ProfiledTopology), _p(_i)], _st),
@@ -296,6 +297,12 @@ class SfbPlan:
                                         _stream(stream)), "tag_dense_allreduce")
         return dW
 
+    def ps_sync(self, dW, root, stream=None):
+        """Replicate-with-PS: reduce to `root` (PreMulSum 1/(nB)) and broadcast back, in place."""
+        _check(_lib.tag_ps_sync(self._h, _dev(dW, self.out_torch, (self.M, self.N), "dW"), root,
+                                _stream(stream)), "tag_ps_sync")
+        return dW
+
     def sgd_step(self, dW, W, v, stream=None):
         shape = (self.M, self.N)
         _check(_lib.tag_sgd_step(self._h, _dev(dW, torch.float32, shape, "dW"),
@@ -394,8 +401,9 @@ def _curve(points):
     return Curve(len(pts), b, t), (b, t)
 
 
-def select_profiled(layers, n, gather_points, allreduce_points, tensor_flops=0):
-    """Per-layer choice from measured cost curves [(bytes, ns), ...] (tag_sfb_select_profiled)."""
+def select_profiled(layers, n, gather_points, allreduce_points, tensor_flops=0, ps_points=None):
+    """Per-layer choice from measured cost curves [(bytes, ns), ...] (tag_sfb_select_profiled);
+    ps_points (optional) adds the Replicate-with-PS option (SYNC_PS)."""
     layers = list(layers)
     arr = (LayerDesc * max(1, len(layers)))()
     for i, L in enumerate(layers):
@@ -403,11 +411,15 @@ def select_profiled(layers, n, gather_points, allreduce_points, tensor_flops=0):
                            _DT_OF[L.get("grad_dtype", "f32")])
     g, keep_g = _curve(gather_points)
     a, keep_a = _curve(allreduce_points)
-    topo = ProfiledTopology(n, g, a, tensor_flops)
+    if ps_points:
+        ps, keep_p = _curve(ps_points)
+    else:
+        ps, keep_p = Curve(0, None, None), None
+    topo = ProfiledTopology(n, g, a, tensor_flops, ps)
     out = (ctypes.c_int * max(1, len(layers)))()
     _check(_lib.tag_sfb_select_profiled(arr, len(layers), ctypes.byref(topo), out),
            "tag_sfb_select_profiled")
-    del keep_g, keep_a
+    del keep_g, keep_a, keep_p
     return [out[i] for i in range(len(layers))]
 
 

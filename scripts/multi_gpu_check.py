@@ -12,7 +12,8 @@ gradients"):
   5. fp32 toy config (64x32, B=4) <= 1e-5; fp32 -> bf16 wire (pack + in-place gather);
   6. fused SGD-momentum: identical W, v on every rank and equal to the unfused path;
   7. selector decisions identical on every rank and equal to the oracle's;
-  11. the bias gradient from the gathered dY_all: bit-exact on integers, identical on all ranks.
+  11. the bias gradient from the gathered dY_all: bit-exact on integers, identical on all ranks;
+  12. Replicate-with-PS (reduce to a round-robin PS + broadcast) equals the dense route.
 Rank 0 prints one JSON line with the results; exit code 0 iff every check passed.
 """
 import hashlib
@@ -222,6 +223,33 @@ def main():
     g.close()
     for p in plans:
         p.close()
+
+    # 12: Replicate-with-PS: reduce to a round-robin PS, broadcast back — equals the
+    #     oracle's dense route, identical on every rank, for every choice of root
+    M, N, B = 4096, 1000, 32
+    X, dY = synth.factors(63, 0, rank, M, N, B, "relu", "softmax_onehot")
+    plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32")
+    Xd, dYd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(dY).to(torch.bfloat16).cuda()
+    Xall, dYall = synth.all_factors(63, 0, n, M, N, B, "relu", "softmax_onehot")
+    Xe = torch.from_numpy(Xall).to(torch.bfloat16).double().numpy()
+    dYe = torch.from_numpy(dYall).to(torch.bfloat16).double().numpy()
+    ref = oracle.dense_dw(Xe, dYe)
+    okp = True
+    for root in range(n):
+        dW = torch.empty(M, N, device="cuda")
+        plan.local_grad(Xd, dYd, dW)
+        plan.ps_sync(dW, root)
+        torch.cuda.synchronize()
+        hashes = tdist.all_gather_object(digest(dW))
+        e = rel_fro(dW.cpu().numpy(), ref)
+        okp = okp and len(set(hashes)) == 1 and e <= 1e-5
+    try:
+        plan.ps_sync(torch.empty(M, N, device="cuda"), n)
+        okp = False
+    except tag.TagError as ex:
+        okp = okp and ex.status == tag.ERR_INVALID_ARG
+    record("ps_sync", okp, rel_fro=e)
+    plan.close()
 
     # 7: selector identical on all ranks and equal to the oracle
     lays = [dict(M=L.M, N=L.N, B=L.B) for c in (2, 3, 4, 5) for L in synth.CONFIGS[c].layers]

@@ -4,6 +4,7 @@ P:331-334: transfers "starting from 1KB and doubled until 1GB"; SPEC fit_comm S:
 
   gather     x = bytes each rank receives, (n-1) * B(M+N) * 2   -> ns of tag_sfb_gather (NVLink push)
   allreduce  x = gradient bytes M * N * 4                        -> ns of tag_dense_allreduce
+  ps         x = gradient bytes M * N * 4                        -> ns of tag_ps_sync (root 0)
 
 Run under torchrun with n ranks; every point is device-timed on one call after a device barrier
 (median of `--reps`, max over ranks). Rank 0 writes profiles/comm_n{n}.json."""
@@ -49,7 +50,7 @@ def timed(fn):
     return tdist.max_over_ranks(statistics.median(ts[2:])) * 1e6     # ns
 
 
-gather, allreduce = [], []
+gather, allreduce, ps = [], [], []
 x = 4096
 while x <= args.max_gather:
     B = 8
@@ -70,12 +71,14 @@ while x <= args.max_allreduce:
     dW = torch.randn(M, N, device="cuda")
     ns = timed(lambda: plan.dense_allreduce(dW, s))
     allreduce.append([M * N * 4, int(round(ns))])
+    ns = timed(lambda: plan.ps_sync(dW, 0, s))
+    ps.append([M * N * 4, int(round(ns))])
     plan.close()
     del dW
     x *= 2
 if rank == 0:
     out = {"n": world, "gpu": torch.cuda.get_device_name(0), "gather": gather,
-           "allreduce": allreduce,
+           "allreduce": allreduce, "ps": ps,
            "how": "scripts/profile_comm.py: one call after tag_comm_barrier, median of reps, max over ranks"}
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     path = os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "profiles", f"comm_n{world}.json")

@@ -150,3 +150,30 @@ def test_select_profiled_errors(tagmod):
         tagmod.select_profiled([dict(M=4, N=4, B=1)], 2, [(2, 1), (1, 2)], [(1, 1), (2, 2)])
     assert tagmod.select_profiled([dict(M=4, N=4, B=1)], 1, [(1, 1), (2, 2)],
                                   [(1, 1), (2, 2)]) == [tagmod.SYNC_NONE]
+
+
+def test_select_profiled_with_ps_bit_exact(tagmod, oracle_mod):
+    """Three-way profiled decision (AllReduce / SFB / Replicate-with-PS) equals the oracle's."""
+    S = oracle_mod.selector
+    rs = np.random.default_rng(33)
+    dt = {2: "bf16", 4: "f32"}
+    seen = set()
+    for _ in range(400):
+        def curve():
+            b = np.cumsum(rs.integers(1, 10 ** 8, int(rs.integers(2, 6)))).tolist()
+            t = rs.integers(1000, 10 ** 7, len(b)).tolist()
+            return list(zip(b, t))
+        g, a, ps = curve(), curve(), curve()
+        n = int(rs.integers(2, 9))
+        lays = [dict(M=int(rs.integers(1, 30000)), N=int(rs.integers(1, 30000)),
+                     B=int(rs.integers(1, 2048)), e_w=int(rs.choice([2, 4])),
+                     e_g=int(rs.choice([2, 4]))) for _ in range(4)]
+        got = tagmod.select_profiled([dict(M=l["M"], N=l["N"], B=l["B"], factor_dtype=dt[l["e_w"]],
+                                           grad_dtype=dt[l["e_g"]]) for l in lays], n, g, a, 0, ps)
+        want = [S.select_profiled(l, n, g, a, 0, ps) for l in lays]
+        assert got == want
+        seen.update(got)
+    assert seen == {tagmod.SYNC_ALLREDUCE, tagmod.SYNC_SFB, tagmod.SYNC_PS}
+    with pytest.raises(tagmod.TagError):
+        tagmod.select_profiled([dict(M=4, N=4, B=1)], 2, [(1, 1), (2, 2)], [(1, 1), (2, 2)], 0,
+                               [(2, 1), (1, 2)])                       # PS bytes not increasing

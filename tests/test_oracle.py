@@ -355,3 +355,25 @@ def test_bias_fractions_and_ones(oracle_mod):
     for j in range(N):
         assert abs(Fraction(got[j]) - want[j]) <= Fraction(1, 10 ** 14)
     assert np.array_equal(oracle_mod.sfb_bias(np.ones((n, B, N))), np.ones(N))
+
+
+def test_profiled_ps_option(oracle_mod):
+    """Replicate-with-PS in the profiled selector: a PS curve equal to the AllReduce
+    curve never wins (tie keeps AllReduce), one strictly below both wins, and one equal to SFB's
+    cost keeps SFB; without a PS curve the two-way rule is unchanged."""
+    S = oracle_mod.selector
+    lay = dict(M=4096, N=4096, B=32, e_w=2, e_g=4)
+    G = 4096 * 4096 * 4
+    gather = [(1, 10_000), (10 ** 9, 10 ** 9)]          # cheap SFB
+    ar = [(1, 10_000), (10 ** 9, 2 * 10 ** 9)]
+    assert S.select_profiled(lay, 2, gather, ar) == S.CHOICE_SFB
+    assert S.select_profiled(lay, 2, gather, ar, 0, ar) == S.CHOICE_SFB
+    t_sfb = S.curve_ns(gather, 1 * 32 * (4096 + 4096) * 2)
+    cheap_ps = [(0, 0), (2 * G, 2 * (t_sfb - 1))]        # ps(G) = t_sfb - 1 < t_sfb
+    assert S.curve_ns(cheap_ps, G) == t_sfb - 1
+    assert S.select_profiled(lay, 2, gather, ar, 0, cheap_ps) == S.CHOICE_PS
+    tie_ps = [(0, 0), (2 * G, 2 * t_sfb)]
+    assert S.select_profiled(lay, 2, gather, ar, 0, tie_ps) == S.CHOICE_SFB
+    expensive_gather = [(1, 10 ** 9), (10 ** 9, 10 ** 10)]
+    assert S.select_profiled(lay, 2, expensive_gather, ar, 0, ar) == S.CHOICE_ALLREDUCE
+    assert S.select_profiled(lay, 1, gather, ar, 0, cheap_ps) == S.CHOICE_NONE
