@@ -101,6 +101,7 @@ struct tag_plan_s {
     size_t win_buf_bytes = 0;      // one buffer = K*(M+N)*e_w
     size_t win_flag_off = 0;       // two u32 arrival counters (one per buffer parity)
     uint32_t flag_total[2] = {0, 0};   // counter value after every fused call so far, per parity
+    uint32_t local_total[2] = {0, 0};  // local (hierarchical publish) counter, per parity
     int parity = 0;
     void* lx = nullptr;            // local cast scratch for tag_local_grad (B x M, B x N wire)
     void* ldy = nullptr;
@@ -343,11 +344,23 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
             a[i].M = rc;
         }
     }
-    // every CTA of every rank adds 1 per layer: the counter grows by n * grid per call
-    const uint32_t inc = static_cast<uint32_t>(c->nranks) * static_cast<uint32_t>(recon_tc_grid(a, count));
+    // hierarchical publish (default): the last CTA of every rank adds 1 per layer, so each
+    // counter grows by n per call; per-CTA publish (TAG_FUSED_HIER=0): by n * grid
+    static const bool hier = [] {
+        const char* e = std::getenv("TAG_FUSED_HIER");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    const uint32_t grid = static_cast<uint32_t>(recon_tc_grid(a, count));
+    const uint32_t inc = static_cast<uint32_t>(c->nranks) * (hier ? 1u : grid);
     for (int i = 0; i < count; ++i) a[i].flag_target = plans[i]->flag_total[plans[i]->parity] + inc;
+    tag_plan_s* p0 = plans[0];
     FusedGather fg{c->nranks, c->rank, c->mc_base,
-                   plans[0]->d.in_dtype == TAG_F32 && plans[0]->d.wire_dtype == TAG_BF16};
+                   plans[0]->d.in_dtype == TAG_F32 && plans[0]->d.wire_dtype == TAG_BF16,
+                   hier ? reinterpret_cast<uint32_t*>(static_cast<char*>(p0->win_base) +
+                                                      p0->win_flag_off + 8 + 4 * p0->parity)
+                        : nullptr,
+                   p0->local_total[p0->parity] + grid};
+    if (hier) p0->local_total[p0->parity] += grid;
     TAG_TRY(launch_recon_tc_group(a, count, s, &fg));
     for (int i = 0; i < count; ++i) {
         tag_plan_s* p = plans[i];

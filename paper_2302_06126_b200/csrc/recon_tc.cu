@@ -121,6 +121,8 @@ struct GroupParams {
     char* mc_base;         // FUSED: NVLS multicast base of the windows, or nullptr (unicast)
     int dbg;               // TAG_FUSED_DEBUG (profiling only): 1 no push/wait, 2 no wait, 3 stamps
     int cast;              // FUSED: the sources are fp32, cast to bf16 (RNE) on the way out
+    uint32_t* local_ctr;   // FUSED: hierarchical publish (FusedGather::local_ctr) or nullptr
+    uint32_t local_target;
 };
 
 struct TileRef {
@@ -215,10 +217,21 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
         }
     }
     // One system-scope release for the whole slice (a fence per layer costs a NVLink round trip
-    // each), then relaxed increments of every layer's arrival counter on every peer.
+    // each), then relaxed increments of every layer's arrival counter on every peer — by every
+    // CTA, or (hierarchical) only by the last CTA of this rank to arrive on a local counter,
+    // which cuts the remote atomics landing on each counter from n * grid to n.
     __syncthreads();
     if (threadIdx.x == 0) {
         asm volatile("fence.acq_rel.sys;" ::: "memory");
+        if (gp.local_ctr != nullptr) {
+            uint32_t old;
+            asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
+                         : "=r"(old) : "l"(gp.local_ctr) : "memory");
+            if (old + 1 != gp.local_target) return;        // not the last CTA of this rank
+            // every other CTA's slice was released at system scope before its local add,
+            // which this acquire observed; make that cumulative for the peers
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
+        }
         for (int li = 0; li < gp.count; ++li) {
             if (mc != nullptr) {
                 asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], 1;"
@@ -772,6 +785,8 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     }();
     gp.dbg = dbg;
     gp.cast = FUSED && fg->cast ? 1 : 0;
+    gp.local_ctr = FUSED ? fg->local_ctr : nullptr;
+    gp.local_target = FUSED ? fg->local_target : 0;
     auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED, X3>;
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {

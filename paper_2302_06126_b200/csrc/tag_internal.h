@@ -54,6 +54,10 @@ struct FusedGather {
     int me;                // LSA rank (== comm rank)
     void* mc_base;         // NVLS multicast base (multimem.st to every GPU at once), or nullptr
     bool cast;             // sources are fp32, the wire is bf16 (RNE cast inside the push)
+    // hierarchical publish: CTAs count themselves on a local counter; the last one of this rank
+    // adds 1 to every layer's counter on every peer (n remote atomics per layer, not n * grid)
+    uint32_t* local_ctr;   // device address (this rank's window) or nullptr = per-CTA publish
+    uint32_t local_target; // local counter value after this launch's CTAs have all arrived
 };
 
 // Tensor-core path (tcgen05 + TMEM + TMA). Requires 16-byte aligned rows (see recon_tc_ok).
