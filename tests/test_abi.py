@@ -177,3 +177,34 @@ def test_select_profiled_with_ps_bit_exact(tagmod, oracle_mod):
     with pytest.raises(tagmod.TagError):
         tagmod.select_profiled([dict(M=4, N=4, B=1)], 2, [(1, 1), (2, 2)], [(1, 1), (2, 2)], 0,
                                [(2, 1), (1, 2)])                       # PS bytes not increasing
+
+
+def _build_c_example(tmp_path):
+    import subprocess
+    exe = str(tmp_path / "c_abi_example")
+    lib_dir = os.path.join(ROOT, "paper_2302_06126_b200")
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    "-I", "/usr/local/cuda/include", os.path.join(ROOT, "examples", "c_abi_example.c"),
+                    "-o", exe, "-L", lib_dir, "-ltag", f"-Wl,-rpath,{lib_dir}",
+                    "-L", "/usr/local/cuda/lib64", "-lcudart"], check=True)
+    return exe
+
+
+def test_c_program_uses_the_abi(tmp_path, tagmod):
+    """include/tag.h is plain C11 and libtag links into a C program; its host-only calls
+    (selector, ILP, argument validation) run without a GPU."""
+    import subprocess
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([exe, "--host"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "fc6 -> SFB" in r.stdout and "objective = -9.700e-04" in r.stdout
+
+
+@pytest.mark.gpu
+def test_c_program_sync_on_gpu(tmp_path, tagmod):
+    """The same C program runs one SFB sync on GPU 0 and checks every element exactly."""
+    import subprocess
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 mismatches" in r.stdout
