@@ -13,7 +13,8 @@ gradients"):
   6. fused SGD-momentum: identical W, v on every rank and equal to the unfused path;
   7. selector decisions identical on every rank and equal to the oracle's;
   11. the bias gradient from the gathered dY_all: bit-exact on integers, identical on all ranks;
-  12. Replicate-with-PS (reduce to a round-robin PS + broadcast) equals the dense route.
+  12. Replicate-with-PS (reduce to a round-robin PS + broadcast) equals the dense route;
+  1b. K = nB = 256 (north_star's n = 8 point) through the fused CTA-pair kernel, bit exact.
 Rank 0 prints one JSON line with the results; exit code 0 iff every check passed.
 """
 import hashlib
@@ -83,6 +84,17 @@ def main():
         ed = rel_fro(dense.cpu().numpy(), ref)
         record(f"vgg_{M}x{N}", len(set(hashes)) == 1 and e <= 1e-5 and ed <= 1e-5,
                rel_fro=e, dense_rel_fro=ed, identical_ranks=len(set(hashes)) == 1)
+
+    # 1b: K = n*B >= 192 takes the CTA-pair (cta_group::2) fused kernel — the n = 8 shape of
+    #     north_star's target (K = 256) at n = 2 and 4; integer inputs, bit exact
+    for M, N in ((4096, 4096), (520, 264)):
+        Bp = 256 // n
+        dW, dense, hashes, Xall, dYall, Xe, dYe = run(64, M % 7, M, N, Bp, "int3", "int3", "bf16", "bf16", "f32")
+        S = oracle.sfb_sum(Xall, dYall)
+        want = S.astype(np.float32) * np.float32(1.0 / (n * Bp))
+        got = dW.cpu().numpy()
+        record(f"pairs_K256_{M}x{N}", np.array_equal(got.view(np.uint32), want.view(np.uint32))
+               and len(set(hashes)) == 1, max_abs=float(np.abs(got - want).max()))
 
     # 2: integer inputs, bit exact (odd tile edges: 520 x 264)
     dW, dense, hashes, Xall, dYall, Xe, dYe = run(60, 0, 520, 264, 24, "int3", "int3", "bf16", "bf16", "f32")
