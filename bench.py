@@ -188,6 +188,53 @@ def virtual_n_recon(tag, comm, cfg, nv, stream, flush_l2, start_events, peaks, i
     return out
 
 
+def projected_n8(tag, comm, cfg, stream, flush_l2, start_events, dw_bytes, iters=20):
+    """SURVEY d-1b "n = 8 without 8 GPUs": the bucket's reconstruction timed at K = 8B on this GPU
+    (virtual replicas, one grouped launch) plus the factor gather read off the measured n = 4
+    curve (profiles/comm_n4.json) at the n = 8 ingress (7 * B(M+N) * 2 bytes). Labelled
+    projected, never measured."""
+    prof = os.path.join(ROOT, "profiles", "comm_n4.json")
+    if not os.path.exists(prof) or cfg.sgd:
+        return None
+    curve = json.load(open(prof))["gather"]
+    plans, Xs, dYs, dWs = [], [], [], []
+    for li, L in enumerate(cfg.layers):
+        K = 8 * L.B
+        X, dY = synth.all_factors(cfg.cid, li, 8, L.M, L.N, L.B, L.x_dist, L.dy_dist)
+        plans.append(tag.SfbPlan(comm, L.M, L.N, K, "bf16", "bf16", cfg.out_dtype))
+        Xs.append(torch.from_numpy(X.reshape(K, L.M)).to(torch.bfloat16).cuda())
+        dYs.append(torch.from_numpy(dY.reshape(K, L.N)).to(torch.bfloat16).cuda())
+        dWs.append(torch.empty(L.M, L.N, dtype=torch.float32 if cfg.out_dtype == "f32" else torch.bfloat16,
+                               device="cuda"))
+    g = tag.SfbGroup(plans)
+    g.gather(Xs, dYs, stream)
+    for _ in range(3):
+        g.reconstruct(dWs, stream)
+    ts = []
+    for _ in range(iters):
+        evs = start_events(2)
+        g.reconstruct(dWs, stream)
+        evs[1].record(stream)
+        torch.cuda.synchronize()
+        ts.append(evs[0].elapsed_time(evs[1]))
+    g.close()
+    for p in plans:
+        p.close()
+    rec_us = statistics.median(ts) * 1e3
+    ingress = sum(7 * L.B * (L.M + L.N) * 2 for L in cfg.layers)
+    i = 0
+    while i + 2 < len(curve) and ingress > curve[i + 1][0]:
+        i += 1
+    (b0, t0), (b1, t1) = curve[i], curve[i + 1]
+    gather_us = (t0 + (ingress - b0) * (t1 - t0) / (b1 - b0)) / 1e3
+    step_us = rec_us + gather_us
+    return {"label": "projected n = 8 (not measured): virtual-n bucket reconstruction + gather "
+                     "from the n = 4 curve", "K": 8 * cfg.layers[0].B,
+            "recon_bucket_us": round(rec_us, 2), "gather_ingress_MB": round(ingress / 1e6, 2),
+            "gather_us_from_n4_curve": round(gather_us, 2), "step_us": round(step_us, 2),
+            "value_GBps": round(8 * dw_bytes / (step_us * 1e-6) / 1e9, 1)}
+
+
 def config_json(cfg, n, args):
     return {"workload": f"{cfg.name} sync (configs[{cfg.cid - 1}]), n={n}",
             "layers": [f"{L.name} {L.M}x{L.N}" for L in cfg.layers], "rows_per_gpu": cfg.layers[0].B,
@@ -363,6 +410,11 @@ def main():
                                 else ([], []))
 
     t_step_ms = tdist.max_over_ranks(statistics.mean(steps_ms))
+    qs = statistics.quantiles(steps_ms, n=10) if len(steps_ms) >= 2 else [steps_ms[0]] * 9
+    step_stats = {"p10_ms": round(tdist.max_over_ranks(qs[0]), 4),
+                  "p50_ms": round(tdist.max_over_ranks(statistics.median(steps_ms)), 4),
+                  "p90_ms": round(tdist.max_over_ranks(qs[8]), 4),
+                  "mean_ms": round(t_step_ms, 4), "steps": len(steps_ms)}
     dw_bytes = sum(l["L"].M * l["L"].N * ESIZE[cfg.out_dtype] for l in layers)
     value = n * dw_bytes / (t_step_ms * 1e-3) / 1e9
 
@@ -520,9 +572,10 @@ def main():
     # ---------------------------------------------------------------- virtual n = 8 (1 GPU)
     # north_star's target point is fc6 at n = 8 (K = 256); with one GPU the reconstruction of that
     # point is timed on K = 8*32 stacked factor rows (identical contraction and alpha = 1/(8B))
-    virt = None
+    virt = proj8 = None
     if n == 1 and not args.no_virtual:
         virt = virtual_n_recon(tag, comm, cfg, 8, stream, flush_l2, start_events, peaks)
+        proj8 = projected_n8(tag, comm, cfg, stream, flush_l2, start_events, dw_bytes)
 
     clocks = clk.summary()
     cpu = None
@@ -536,7 +589,8 @@ def main():
                 "dtype": cfg.wire_dtype, "data": "synthetic", "config": config_json(cfg, n, args),
                 "per_layer": per_layer, "roofline": roofline, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
-                "virtual_n8_recon": virt, "sharded_variant": sharded,
+                "virtual_n8_recon": virt, "projected_n8": proj8, "step_stats": step_stats,
+                "sharded_variant": sharded,
                 "lib": tag.version()}
         print(json.dumps(line), flush=True)
     if group is not None:
