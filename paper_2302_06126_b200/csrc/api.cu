@@ -181,6 +181,21 @@ tag_status_t check_ptrs(const char* fn, std::initializer_list<const void*> ps) {
 
 bool needs_gather_buffers(const tag_sfb_desc_t& d) { return d.n > 1 || d.in_dtype != d.wire_dtype; }
 
+// Every rank's device work up to here is complete and every rank has reached this point: the
+// window of a new plan is zeroed everywhere before any peer can push into it (a late memset
+// would wipe a peer's factors and arrival counters), and on destroy no peer still writes into
+// a window that is about to be freed.
+tag_status_t quiesce_all_ranks(tag_comm_s* c, const char* where) {
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, where);
+    if (c->nranks > 1 && c->devcomm && c->lsa_all) {
+        TAG_TRY(launch_comm_barrier(c->devcomm, COMM_BARRIER_INDEX, nullptr));
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return cuda_fail(e, where);
+    }
+    return TAG_OK;
+}
+
 // a1 + a2: leaves the operands of the reconstruction in plan->src_x / src_dy
 tag_status_t do_gather(tag_plan_s* p, const void* X, const void* dY, cudaStream_t s) {
     const tag_sfb_desc_t& d = p->d;
@@ -526,6 +541,12 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
             cleanup();
             return cuda_fail(e, "tag_sfb_plan: cudaMemset(window)");
         }
+        // the zeroed window and arrival counters must exist on EVERY rank before any rank pushes
+        tag_status_t qs = quiesce_all_ranks(c, "tag_sfb_plan: window initialisation");
+        if (qs != TAG_OK) {
+            cleanup();
+            return qs;
+        }
         if (d->in_dtype != d->wire_dtype) {
             e = cudaMalloc(&p->lx, static_cast<size_t>(d->B * d->M) * ew);
             if (e == cudaSuccess) e = cudaMalloc(&p->ldy, static_cast<size_t>(d->B * d->N) * ew);
@@ -583,6 +604,7 @@ tag_status_t tag_sfb_plan_info(tag_sfb_plan_t p, tag_plan_info_t* out) {
 tag_status_t tag_sfb_plan_destroy(tag_sfb_plan_t p) {
     if (!p) return TAG_OK;
     set_device(p->comm);
+    if (p->win) quiesce_all_ranks(p->comm, "tag_sfb_plan_destroy");   // no peer writes in flight
     if (p->has_premul) ncclRedOpDestroy(p->premul, p->comm->nccl);
     if (p->win) ncclCommWindowDeregister(p->comm->nccl, p->win);
     if (p->win_base) ncclMemFree(p->win_base);

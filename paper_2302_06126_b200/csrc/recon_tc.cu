@@ -42,7 +42,8 @@ namespace {
 constexpr int BM = 128;                  // UMMA M (TMEM lanes)
 constexpr int NUM_EPI_WARPS = 8;
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;   // 320
-constexpr int EPI_BUF_BYTES = 2 * 32 * 128;  // 2 x (32 rows x 128 B) transpose buffers per warp
+constexpr int EPI_CHUNK_BYTES = 32 * 128;    // one 32 rows x 128 B transpose buffer
+constexpr int SMEM_MAX = 232448;              // 227 KB of dynamic shared memory per CTA
 constexpr int TMEM_COLS = 512;
 
 // CTAS = 2: a CTA pair on one TPC runs tcgen05 cta_group::2 — UMMA M = 256 (128 rows of A in
@@ -54,7 +55,9 @@ constexpr int TMEM_COLS = 512;
 // issues hi*hi + hi*lo + lo*hi, which recovers ~fp32 accuracy (the dropped lo*lo and the tf32
 // truncations are ~2^-21 relative per product) at 3 MMAs per step — free while the epilogue's
 // HBM write binds. Stages carry 16 fp32 rows (32-element MN chunks of 128 B) of all four operands.
-template <int BN, int CTAS, bool X3 = false>
+// EP = epilogue chunks staged per round (2 for the fp32 E1 store, 1 for bf16 / E2 / X3), which
+// sizes the per-warp transpose buffers; the operand ring takes the rest of shared memory.
+template <int BN, int CTAS, bool X3 = false, int EP = 2>
 struct Cfg {
     // X3 keeps two accumulators per tile: hi*hi, and the small hi*lo + lo*hi terms apart, so the
     // big accumulator sees K/8 additions instead of 3K/8 (the tensor core's fp32 accumulation
@@ -62,7 +65,10 @@ struct Cfg {
     static constexpr int ACC_COLS = X3 ? 2 * BN : BN;     // TMEM columns per tile
     static constexpr int ACC = TMEM_COLS / ACC_COLS;      // accumulator buffers in TMEM
     static constexpr int ELEMS = X3 ? 32 : 64;            // MN elements per 128-byte chunk
-    static constexpr int BK = X3 ? 16 : 32;               // factor rows per pipeline stage
+    // factor rows per pipeline stage. CTA pairs (K >= 192) load 64-row boxes: 8 KB per TMA
+    // request instead of 4 KB (fc6 at K = 256, bf16 dW: 68.3 -> 58.2 us; the per-request cost,
+    // not bytes, paced the operand stream)
+    static constexpr int BK = X3 ? 16 : (CTAS == 2 ? 64 : 32);
     static constexpr int KMMA = X3 ? 8 : 16;              // K per tcgen05.mma
     static constexpr int CHUNK_BYTES = BK * 128;          // one 128-byte-wide MN chunk of BK rows
     static constexpr int A_CHUNKS = BM / ELEMS;
@@ -74,10 +80,13 @@ struct Cfg {
     static constexpr int A_BYTES = HALVES * A_CHUNKS * CHUNK_BYTES;
     static constexpr int B_BYTES = HALVES * B_CHUNKS * CHUNK_BYTES;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    // pairs: 8 stages (VGG bucket at K = 256: 104 -> 99 us vs 6; 9-10 no better)
-    static constexpr int STAGES = X3 ? 4 : (CTAS == 2 ? 8 : (BN == 256 ? 6 : 8));
+    static constexpr int EPI_BUF_BYTES = EP * EPI_CHUNK_BYTES;   // per epilogue warp
     static constexpr int EPI_BYTES = NUM_EPI_WARPS * EPI_BUF_BYTES;
     static constexpr int BAR_BYTES = 256;
+    // as many stages as fit, at most 8 (BN = 128: 8; BN = 256 one CTA: 6; pairs: 5, or 6 with a
+    // one-chunk epilogue)
+    static constexpr int FIT = (SMEM_MAX - 1024 - EPI_BYTES - BAR_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES = X3 ? 4 : (FIT < 8 ? FIT : 8);
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
     // instruction descriptor: D f32, A/B bf16 (kind::f16) or tf32 (kind::tf32), both MN-major,
     // N = BN, M = 128 * CTAS.
@@ -265,8 +274,10 @@ template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const int me)
 {
-    using C = Cfg<BN, CTAS, X3>;
+    constexpr int EP = OUT_BF16 || SGD || X3 ? 1 : 2;   // epilogue chunks per round
+    using C = Cfg<BN, CTAS, X3, EP>;
     static_assert(!X3 || (CTAS == 1 && !FUSED), "3xTF32: single-CTA tiles, staged gather");
+    static_assert(C::SMEM <= SMEM_MAX, "shared memory budget");
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the SWIZZLE_128B atoms
     const uint32_t base = (ptx::smem_addr(smem_raw) + 1023u) & ~1023u;
@@ -441,12 +452,12 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
         const int ew = warp - 2;                 // 0..7
         const int quad = warp & 3;               // TMEM lane quadrant this warp may access
         const int half = ew >> 2;                // which half of the tile's columns
-        const uint32_t sbuf = s_epi + ew * EPI_BUF_BYTES;
+        const uint32_t sbuf = s_epi + ew * C::EPI_BUF_BYTES;
         constexpr int ESZ = OUT_BF16 ? 2 : 4;
         constexpr int COLS_PER_CHUNK = 128 / ESZ;               // 128 bytes of output per row
         constexpr int CHUNKS = (BN / 2) / COLS_PER_CHUNK;
         constexpr int VEC = 16 / ESZ;                           // output elements per 16 B
-        constexpr int PAIR = OUT_BF16 || SGD || X3 ? 1 : 2;     // chunks staged per round
+        constexpr int PAIR = EP;                                // chunks staged per round
         const int sub = lane >> 3;               // row within a 4-row group (write-out phase)
         const int cj = lane & 7;                 // 16-byte column slot (write-out phase)
         int acc = 0;
@@ -731,7 +742,7 @@ bool big_tiles(const ReconArgs* a, int count) {
 
 template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3 = false>
 tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
-    using C = Cfg<BN, CTAS, X3>;
+    using C = Cfg<BN, CTAS, X3, (OUT_BF16 || SGD || X3 ? 1 : 2)>;
     GroupParams gp;
     std::memset(&gp, 0, sizeof gp);
     int tiles = 0;
