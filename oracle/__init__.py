@@ -8,7 +8,7 @@ method's arithmetic.
 
 Contents
   tag_oracle.c  fp64 dense route, SFB route, per-entry sums, bias gradient (both routes),
-                SGD-momentum, RNE bf16 cast (plain C)
+                SGD-momentum, Adam, RNE bf16 cast (plain C)
   selector.py   exact-integer / Fraction selector, byte counts, ring-AllReduce and ILP formulas
 
 Parity status: every function here is pinned by tests/test_oracle.py against values the paper or
@@ -34,7 +34,7 @@ def build(force=False):
     if not force and os.path.exists(_SO) and os.path.getmtime(_SO) >= os.path.getmtime(_SRC):
         return _SO
     cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
-           "-std=c11", "-o", _SO + ".tmp", _SRC]
+           "-std=c11", "-o", _SO + ".tmp", _SRC, "-lm"]
     subprocess.check_call(cmd)
     os.replace(_SO + ".tmp", _SO)
     return _SO
@@ -57,6 +57,8 @@ def _load():
         lib.oracle_sgd_momentum.restype = None
         lib.oracle_cast_bf16.argtypes = [i64, p, p]
         lib.oracle_cast_bf16.restype = None
+        lib.oracle_adam.argtypes = [i64, p, p, p, p] + [ctypes.c_double] * 5 + [i64]
+        lib.oracle_adam.restype = None
         for name in ("oracle_dense_bias_sum", "oracle_sfb_bias_sum"):
             fn = getattr(lib, name)
             fn.argtypes = [i64, i64, i64, p, p]
@@ -164,3 +166,12 @@ def sfb_bias(dY):
     """db = S_b / (nB) by the SFB route."""
     n, B, _ = np.shape(dY)
     return sfb_bias_sum(dY) / float(n * B)
+
+
+def adam(dW, W, m, v, lr, b1, b2, eps, wd, t):
+    """One Adam step (torch.optim.Adam semantics, step t >= 1) in fp64; returns (W', m', v')."""
+    dW = _f64(dW).ravel()
+    W2, m2, v2 = (_f64(x).ravel().copy() for x in (W, m, v))
+    _load().oracle_adam(dW.size, _ptr(dW), _ptr(W2), _ptr(m2), _ptr(v2), lr, b1, b2, eps, wd, t)
+    shape = np.shape(W)
+    return W2.reshape(shape), m2.reshape(shape), v2.reshape(shape)

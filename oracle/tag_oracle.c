@@ -187,3 +187,25 @@ void oracle_sfb_bias_sum(int64_t n, int64_t B, int64_t N, const double* dY_all, 
     for (int64_t k = 0; k < K; ++k)
         for (int64_t j = 0; j < N; ++j) S[j] += dY_all[k * N + j];
 }
+
+/* ---------------------------------------------------------------------------------------------
+ * Adam applied to the reconstructed gradient (the optimizer the paper trains with, "Adam
+ * optimizer"; R22: torch.optim.Adam semantics, L2 weight decay folded into g,
+ * bias-corrected moments, step t >= 1):
+ *   g  = dW + wd * W
+ *   m' = b1 * m + (1 - b1) * g
+ *   v' = b2 * v + (1 - b2) * g * g
+ *   W' = W - lr * (m' / (1 - b1^t)) / (sqrt(v' / (1 - b2^t)) + eps)
+ * ------------------------------------------------------------------------------------------- */
+#include <math.h>
+void oracle_adam(int64_t len, const double* dW, double* W, double* m, double* v, double lr,
+                 double b1, double b2, double eps, double wd, int64_t t)
+{
+    const double bc1 = 1.0 - pow(b1, (double)t), bc2 = 1.0 - pow(b2, (double)t);
+    for (int64_t i = 0; i < len; ++i) {
+        const double g = dW[i] + wd * W[i];
+        m[i] = b1 * m[i] + (1.0 - b1) * g;
+        v[i] = b2 * v[i] + (1.0 - b2) * g * g;
+        W[i] = W[i] - lr * (m[i] / bc1) / (sqrt(v[i] / bc2) + eps);
+    }
+}

@@ -377,3 +377,31 @@ def test_profiled_ps_option(oracle_mod):
     expensive_gather = [(1, 10 ** 9), (10 ** 9, 10 ** 10)]
     assert S.select_profiled(lay, 2, expensive_gather, ar, 0, ar) == S.CHOICE_ALLREDUCE
     assert S.select_profiled(lay, 1, gather, ar, 0, cheap_ps) == S.CHOICE_NONE
+
+
+# ------------------------------------------------------------------ Adam (R22)
+def test_adam_first_step_closed_form(oracle_mod):
+    """t = 1: the bias corrections undo the (1 - b) factors, so W1 = W0 - lr g / (|g| + eps)."""
+    rs = np.random.default_rng(71)
+    g = rs.standard_normal(1000)
+    W0 = rs.standard_normal(1000)
+    W1, m1, v1 = oracle_mod.adam(g, W0, np.zeros(1000), np.zeros(1000), 1e-3, 0.9, 0.999, 1e-8, 0.0, 1)
+    np.testing.assert_allclose(m1, 0.1 * g, rtol=1e-15)
+    np.testing.assert_allclose(v1, 0.001 * g * g, rtol=1e-14)
+    np.testing.assert_allclose(W1, W0 - 1e-3 * g / (np.abs(g) + 1e-8), rtol=1e-12, atol=1e-15)
+
+
+def test_adam_matches_torch_optim(oracle_mod):
+    """Three steps against torch.optim.Adam in float64 (an independent implementation), with
+    weight decay; the gradient changes every step."""
+    rs = np.random.default_rng(72)
+    W = rs.standard_normal((16, 8))
+    p = torch.nn.Parameter(torch.from_numpy(W.copy()))
+    opt = torch.optim.Adam([p], lr=3e-3, betas=(0.8, 0.95), eps=1e-6, weight_decay=0.01)
+    m, v = np.zeros_like(W), np.zeros_like(W)
+    for t in range(1, 4):
+        g = rs.standard_normal(W.shape)
+        p.grad = torch.from_numpy(g.copy())
+        opt.step()
+        W, m, v = oracle_mod.adam(g, W, m, v, 3e-3, 0.8, 0.95, 1e-6, 0.01, t)
+        np.testing.assert_allclose(W, p.detach().numpy(), rtol=1e-12, atol=1e-14)
