@@ -97,7 +97,8 @@ static int gpu_part(void) {
     }
     tag_comm_t comm = NULL;
     CHECK_TAG(tag_comm_create(NULL, 1, 0, 0, &comm));
-    tag_sfb_desc_t desc = {M, N, B, 1, TAG_BF16, TAG_BF16, TAG_F32, 0, 0.f, 0.f, 0.f};
+    tag_sfb_desc_t desc = {.M = M, .N = N, .B = B, .n = 1, .in_dtype = TAG_BF16,
+                           .wire_dtype = TAG_BF16, .out_dtype = TAG_F32};
     tag_sfb_plan_t plan = NULL;
     CHECK_TAG(tag_sfb_plan(comm, &desc, &plan));
     void *dx, *dy, *dw;

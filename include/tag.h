@@ -122,7 +122,10 @@ typedef struct {
                              /* F32->BF16 (RNE cast in the pack kernel, DESIGN R11)         */
     tag_dtype_t out_dtype;   /* dtype of dW_out (F32 default; BF16 = RNE of the fp32 value) */
     int fuse_sgd;            /* 1: tag_sfb_sync_sgd applies SGD-momentum in the epilogue    */
-    float lr, momentum, weight_decay; /* SGD hyper-parameters, frozen in the plan (R14)     */
+    float lr, momentum, weight_decay; /* optimizer hyper-parameters, frozen in the plan (R14) */
+    int fuse_adam;           /* 1: tag_sfb_sync_adam applies Adam in the epilogue (R22);     */
+                             /* exclusive with fuse_sgd; uses lr and weight_decay too        */
+    float beta1, beta2, eps; /* Adam hyper-parameters (also read by tag_adam_step)           */
 } tag_sfb_desc_t;
 
 /* COLLECTIVE. Validates `desc`, allocates the gather buffers (n*B*M and n*B*N elements of the
@@ -176,6 +179,15 @@ tag_status_t tag_sfb_reconstruct(tag_sfb_plan_t plan, void* dW_out, tag_stream_t
  * dW_out may be NULL (then dW is never written to HBM). Requires desc.fuse_sgd = 1. */
 tag_status_t tag_sfb_sync_sgd(tag_sfb_plan_t plan, const void* X, const void* dY, float* W,
                               float* v, void* dW_out, tag_stream_t stream);
+
+/* COLLECTIVE (n > 1). tag_sfb_sync with Adam fused into the epilogue (the optimizer the paper
+ * trains with; torch.optim.Adam semantics, DESIGN R22), step t >= 1 (bias corrections):
+ *   g = dW + wd*W ; m <- b1*m + (1-b1)*g ; v <- b2*v + (1-b2)*g*g ;
+ *   W <- W - (lr/(1-b1^t)) * m / (sqrt(v)/sqrt(1-b2^t) + eps)       (W, m, v: M x N fp32)
+ * dW_out may be NULL. Requires desc.fuse_adam = 1 (and out_dtype F32). Bitwise equal to
+ * tag_sfb_sync followed by tag_adam_step. */
+tag_status_t tag_sfb_sync_adam(tag_sfb_plan_t plan, const void* X, const void* dY, float* W,
+                               float* m, float* v, int64_t step, void* dW_out, tag_stream_t stream);
 
 /* COLLECTIVE (n > 1). End-to-end form with HOST buffers: copies X and dY (pinned or pageable
  * host memory, in_dtype) to plan-owned device staging, runs tag_sfb_sync into plan-owned device
@@ -231,6 +243,11 @@ tag_status_t tag_sfb_group_sync(tag_sfb_group_t group, const void* const* X,
 tag_status_t tag_sfb_group_sync_sgd(tag_sfb_group_t group, const void* const* X,
                                     const void* const* dY, float* const* W, float* const* v,
                                     void* const* dW, tag_stream_t stream);
+/* Same with Adam (all plans fuse_adam = 1 with identical hyper-parameters); m[i], v[i] fp32. */
+tag_status_t tag_sfb_group_sync_adam(tag_sfb_group_t group, const void* const* X,
+                                     const void* const* dY, float* const* W, float* const* m,
+                                     float* const* v, int64_t step, void* const* dW,
+                                     tag_stream_t stream);
 /* Sharded form of tag_sfb_group_sync: dW_shard[i] is plans[i]'s row shard for this rank
  * (tag_sfb_shard_rows). One fused launch when every plan takes the fused path and every shard is
  * non-empty; otherwise one gather + per-plan reconstructions. */
@@ -269,6 +286,10 @@ tag_status_t tag_ps_sync(tag_sfb_plan_t plan, void* dW, int root, tag_stream_t s
  * g = dW + wd*W; v <- momentum*v + g; W <- W - lr*v. dW fp32 (out_dtype must be F32). */
 tag_status_t tag_sgd_step(tag_sfb_plan_t plan, const float* dW, float* W, float* v,
                           tag_stream_t stream);
+/* Unfused Adam step with the plan's beta1 / beta2 / eps / lr / weight_decay (same arithmetic as
+ * the fused epilogue, step t >= 1): W, m, v updated in place from dW (fp32, M x N). */
+tag_status_t tag_adam_step(tag_sfb_plan_t plan, const float* dW, float* W, float* m, float* v,
+                           int64_t step, tag_stream_t stream);
 
 /* ------------------------------------------------------------------------------------------ */
 /* Selector: per-layer SFB vs AllReduce (the paper's SFB ILP, for one MatMul cut)  */

@@ -116,6 +116,8 @@ struct tag_plan_s {
     // fp32 wire on the tensor cores (3xTF32): split [hi ; lo] operands, kpad rows per half
     void* split = nullptr;
     int64_t kpad = 0;
+    // Adam on a path without the fused epilogue: dW staged here, then the unfused Adam kernel
+    float* adam_dw = nullptr;
 };
 
 struct tag_group_s {
@@ -165,6 +167,16 @@ tag_status_t validate_desc(const tag_comm_s* c, const tag_sfb_desc_t* d) {
         return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: bf16 -> fp32 wire is not a supported pair");
     if (d->fuse_sgd != 0 && d->fuse_sgd != 1)
         return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: fuse_sgd must be 0 or 1");
+    if (d->fuse_adam != 0 && d->fuse_adam != 1)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: fuse_adam must be 0 or 1");
+    if (d->fuse_adam && d->fuse_sgd)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: fuse_sgd and fuse_adam are exclusive");
+    if (d->fuse_adam && !(std::isfinite(d->lr) && std::isfinite(d->weight_decay) &&
+                          d->beta1 >= 0.f && d->beta1 < 1.f && d->beta2 >= 0.f && d->beta2 < 1.f &&
+                          d->eps > 0.f && std::isfinite(d->eps)))
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: Adam needs finite lr / wd, betas in [0, 1), eps > 0");
+    if (d->fuse_adam && d->out_dtype != TAG_F32)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: fuse_adam needs out_dtype = F32");
     if (d->fuse_sgd && !(std::isfinite(d->lr) && std::isfinite(d->momentum) &&
                          std::isfinite(d->weight_decay)))
         return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: non-finite SGD hyper-parameter");
@@ -250,8 +262,38 @@ tag_status_t do_gather(tag_plan_s* p, const void* X, const void* dY, cudaStream_
     return TAG_OK;
 }
 
+// Per-call Adam constants (R22), computed in double and rounded once, shared by the fused
+// epilogue and the unfused kernel.
+struct AdamCall {
+    float b1, omb1, b2, omb2, eps, lr_t, isbc2;
+};
+
+AdamCall adam_call(const tag_sfb_desc_t& d, int64_t step) {
+    const double b1 = d.beta1, b2 = d.beta2;
+    const double bc1 = 1.0 - std::pow(b1, static_cast<double>(step));
+    const double bc2 = 1.0 - std::pow(b2, static_cast<double>(step));
+    return AdamCall{d.beta1, static_cast<float>(1.0 - b1), d.beta2, static_cast<float>(1.0 - b2),
+                    d.eps, static_cast<float>(static_cast<double>(d.lr) / bc1),
+                    static_cast<float>(1.0 / std::sqrt(bc2))};
+}
+
+void set_adam(ReconArgs& a, float* Mm, const AdamCall* ad) {
+    a.opt = ad ? 2 : 1;
+    a.Mm = Mm;
+    if (ad) {
+        a.b1 = ad->b1;
+        a.omb1 = ad->omb1;
+        a.b2 = ad->b2;
+        a.omb2 = ad->omb2;
+        a.eps = ad->eps;
+        a.lr_t = ad->lr_t;
+        a.isbc2 = ad->isbc2;
+    }
+}
+
 tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int64_t K,
-                      float alpha, cudaStream_t s) {
+                      float alpha, cudaStream_t s, float* Mm = nullptr,
+                      const AdamCall* adam = nullptr) {
     if (!p->src_x) return fail(TAG_ERR_INVALID_ARG, "reconstruct: no factors gathered on this plan yet");
     ReconArgs a{};
     a.A = p->src_x;
@@ -269,6 +311,7 @@ tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int
     a.lr = p->d.lr;
     a.mu = p->d.momentum;
     a.wd = p->d.weight_decay;
+    if (sgd) set_adam(a, Mm, adam);
     if (p->use_tc && p->d.wire_dtype == TAG_F32) {
         // 3xTF32: split both operands into [hi ; lo] halves of kp rows (pack_sgd.cu), then the
         // kind::tf32 variant of the tensor-core kernel
@@ -282,6 +325,26 @@ tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int
         a.kpad = kp;
     }
     if (p->use_tc && recon_tc_ok(a)) return launch_recon_tc(a, s);
+    if (adam) {
+        // the SIMT kernel has no Adam epilogue: reconstruct dW (into the caller's buffer or the
+        // plan's staging), then the unfused Adam kernel — the same arithmetic (optim.cuh)
+        float* dw = static_cast<float*>(dW);
+        if (!dw) {
+            if (!p->adam_dw) {
+                cudaError_t e = cudaMalloc(&p->adam_dw, static_cast<size_t>(p->d.M * p->d.N) * 4);
+                if (e != cudaSuccess) {
+                    p->adam_dw = nullptr;
+                    return cuda_fail(e, "reconstruct: cudaMalloc(Adam staging)");
+                }
+            }
+            dw = p->adam_dw;
+        }
+        a.C = dw;
+        a.sgd = false;
+        TAG_TRY(launch_recon_simt(a, s));
+        return launch_adam(dw, W, Mm, V, p->d.M * p->d.N, adam->b1, adam->omb1, adam->b2,
+                           adam->omb2, adam->eps, adam->lr_t, adam->isbc2, p->d.weight_decay, s);
+    }
     return launch_recon_simt(a, s);
 }
 
@@ -319,7 +382,8 @@ void shard_range(const tag_plan_s* p, int rank, int64_t* begin, int64_t* cnt) {
 
 tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* X,
                         const void* const* dY, void* const* dW, bool sgd, float* const* W,
-                        float* const* V, cudaStream_t s, bool sharded = false) {
+                        float* const* V, cudaStream_t s, bool sharded = false,
+                        float* const* Mm = nullptr, const AdamCall* adam = nullptr) {
     tag_comm_s* c = plans[0]->comm;
     ReconArgs a[MAX_GROUP];
     for (int i = 0; i < count; ++i) {
@@ -343,6 +407,7 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
         a[i].lr = p->d.lr;
         a[i].mu = p->d.momentum;
         a[i].wd = p->d.weight_decay;
+        if (sgd) set_adam(a[i], Mm ? Mm[i] : nullptr, adam);
         a[i].srcX = X[i];
         a[i].srcY = dY[i];
         a[i].win = p->win;
@@ -605,6 +670,7 @@ tag_status_t tag_sfb_plan_destroy(tag_sfb_plan_t p) {
     if (!p) return TAG_OK;
     set_device(p->comm);
     if (p->win) quiesce_all_ranks(p->comm, "tag_sfb_plan_destroy");   // no peer writes in flight
+    cudaFree(p->adam_dw);
     if (p->has_premul) ncclRedOpDestroy(p->premul, p->comm->nccl);
     if (p->win) ncclCommWindowDeregister(p->comm->nccl, p->win);
     if (p->win_base) ncclMemFree(p->win_base);
@@ -660,6 +726,36 @@ tag_status_t tag_sfb_sync_sgd(tag_sfb_plan_t p, const void* X, const void* dY, f
     if (fusable(p, dW_out)) return fused_sync(&p, 1, &X, &dY, &dW_out, true, &W, &v, s);
     TAG_TRY(do_gather(p, X, dY, s));
     return do_recon(p, dW_out, true, W, v, p->K, p->alpha, s);
+}
+
+tag_status_t tag_sfb_sync_adam(tag_sfb_plan_t p, const void* X, const void* dY, float* W, float* m,
+                               float* v, int64_t step, void* dW_out, tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_adam: NULL plan");
+    if (!p->d.fuse_adam) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_adam: plan has fuse_adam = 0");
+    if (step < 1) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_adam: step must be >= 1");
+    TAG_TRY(check_ptrs("tag_sfb_sync_adam", {X, dY, W, m, v}));
+    if (dW_out) TAG_TRY(check_ptrs("tag_sfb_sync_adam", {dW_out}));
+    TAG_TRY(set_device(p->comm));
+    TAG_TRY(check_async(p->comm));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const AdamCall ad = adam_call(p->d, step);
+    if (fusable(p, dW_out)) return fused_sync(&p, 1, &X, &dY, &dW_out, true, &W, &v, s, false, &m, &ad);
+    TAG_TRY(do_gather(p, X, dY, s));
+    return do_recon(p, dW_out, true, W, v, p->K, p->alpha, s, m, &ad);
+}
+
+tag_status_t tag_adam_step(tag_sfb_plan_t p, const float* dW, float* W, float* m, float* v,
+                           int64_t step, tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_adam_step: NULL plan");
+    if (step < 1) return fail(TAG_ERR_INVALID_ARG, "tag_adam_step: step must be >= 1");
+    if (!(p->d.beta1 >= 0.f && p->d.beta1 < 1.f && p->d.beta2 >= 0.f && p->d.beta2 < 1.f &&
+          p->d.eps > 0.f))
+        return fail(TAG_ERR_INVALID_ARG, "tag_adam_step: the plan's Adam hyper-parameters are unset");
+    TAG_TRY(check_ptrs("tag_adam_step", {dW, W, m, v}));
+    TAG_TRY(set_device(p->comm));
+    const AdamCall ad = adam_call(p->d, step);
+    return launch_adam(dW, W, m, v, p->d.M * p->d.N, ad.b1, ad.omb1, ad.b2, ad.omb2, ad.eps,
+                       ad.lr_t, ad.isbc2, p->d.weight_decay, reinterpret_cast<cudaStream_t>(stream));
 }
 
 tag_status_t tag_sfb_bias_grad(tag_sfb_plan_t p, void* db_out, tag_stream_t stream) {
@@ -837,6 +933,12 @@ tag_status_t tag_sfb_group_create(const tag_sfb_plan_t* plans, int count, tag_sf
                                p->d.weight_decay != plans[0]->d.weight_decay)))
             return fail(TAG_ERR_INVALID_ARG,
                         "tag_sfb_group_create: plans must share fuse_sgd and its hyper-parameters");
+        if (p->d.fuse_adam != plans[0]->d.fuse_adam ||
+            (p->d.fuse_adam && (p->d.lr != plans[0]->d.lr || p->d.beta1 != plans[0]->d.beta1 ||
+                                p->d.beta2 != plans[0]->d.beta2 || p->d.eps != plans[0]->d.eps ||
+                                p->d.weight_decay != plans[0]->d.weight_decay)))
+            return fail(TAG_ERR_INVALID_ARG,
+                        "tag_sfb_group_create: plans must share fuse_adam and its hyper-parameters");
         for (int j = 0; j < i; ++j)
             if (plans[j] == p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_create: duplicate plan");
     }
@@ -902,7 +1004,8 @@ tag_status_t tag_sfb_group_gather(tag_sfb_group_t g, const void* const* X, const
 }
 
 static tag_status_t group_reconstruct(tag_sfb_group_t g, void* const* dW, bool sgd,
-                                      float* const* W, float* const* V, tag_stream_t stream) {
+                                      float* const* W, float* const* V, tag_stream_t stream,
+                                      float* const* Mm = nullptr, const AdamCall* adam = nullptr) {
     const int count = static_cast<int>(g->plans.size());
     for (int i = 0; i < count; ++i) {
         if (!sgd || dW[i]) TAG_TRY(check_ptrs("tag_sfb_group_reconstruct", {dW[i]}));
@@ -932,19 +1035,20 @@ static tag_status_t group_reconstruct(tag_sfb_group_t g, void* const* dW, bool s
         a[i].lr = p->d.lr;
         a[i].mu = p->d.momentum;
         a[i].wd = p->d.weight_decay;
+        if (sgd) set_adam(a[i], Mm ? Mm[i] : nullptr, adam);
         tc = tc && recon_tc_ok(a[i]);
     }
     if (tc) return launch_recon_tc_group(a, count, s);
     for (int i = 0; i < count; ++i)
         TAG_TRY(do_recon(g->plans[i], dW[i], sgd, sgd ? W[i] : nullptr, sgd ? V[i] : nullptr,
-                         g->plans[i]->K, g->plans[i]->alpha, s));
+                         g->plans[i]->K, g->plans[i]->alpha, s, Mm ? Mm[i] : nullptr, adam));
     return TAG_OK;
 }
 
 tag_status_t tag_sfb_group_reconstruct(tag_sfb_group_t g, void* const* dW, tag_stream_t stream) {
     if (!g || !dW) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_reconstruct: NULL argument");
-    if (g->plans[0]->d.fuse_sgd)
-        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_reconstruct: fuse_sgd group, use sync_sgd");
+    if (g->plans[0]->d.fuse_sgd || g->plans[0]->d.fuse_adam)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_reconstruct: fused-optimizer group, use sync_sgd / sync_adam");
     return group_reconstruct(g, dW, false, nullptr, nullptr, stream);
 }
 
@@ -988,13 +1092,40 @@ tag_status_t tag_sfb_group_sync_sgd(tag_sfb_group_t g, const void* const* X, con
     return group_reconstruct(g, dWs, true, W, v, stream);
 }
 
+tag_status_t tag_sfb_group_sync_adam(tag_sfb_group_t g, const void* const* X, const void* const* dY,
+                                     float* const* W, float* const* m, float* const* v,
+                                     int64_t step, void* const* dW, tag_stream_t stream) {
+    if (!g || !X || !dY || !W || !m || !v)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync_adam: NULL argument");
+    if (!g->plans[0]->d.fuse_adam)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync_adam: plans have fuse_adam = 0");
+    if (step < 1) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync_adam: step must be >= 1");
+    const int count = static_cast<int>(g->plans.size());
+    void* none[MAX_GROUP] = {nullptr};
+    void* const* dWs = dW ? dW : none;
+    bool fuse = true;
+    for (int i = 0; i < count; ++i) {
+        TAG_TRY(check_ptrs("tag_sfb_group_sync_adam", {X[i], dY[i], W[i], m[i], v[i]}));
+        if (dWs[i]) TAG_TRY(check_ptrs("tag_sfb_group_sync_adam", {dWs[i]}));
+        fuse = fuse && fusable(g->plans[i], dWs[i]);
+    }
+    TAG_TRY(set_device(g->plans[0]->comm));
+    TAG_TRY(check_async(g->plans[0]->comm));
+    const AdamCall ad = adam_call(g->plans[0]->d, step);
+    if (fuse)
+        return fused_sync(g->plans.data(), count, X, dY, dWs, true, W, v,
+                          reinterpret_cast<cudaStream_t>(stream), false, m, &ad);
+    TAG_TRY(tag_sfb_group_gather(g, X, dY, stream));
+    return group_reconstruct(g, dWs, true, W, v, stream, m, &ad);
+}
+
 tag_status_t tag_sfb_group_sync_sharded(tag_sfb_group_t g, const void* const* X,
                                         const void* const* dY, void* const* dW,
                                         tag_stream_t stream) {
     if (!g || !X || !dY || !dW)
         return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync_sharded: NULL argument");
-    if (g->plans[0]->d.fuse_sgd)
-        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync_sharded: fuse_sgd group");
+    if (g->plans[0]->d.fuse_sgd || g->plans[0]->d.fuse_adam)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync_sharded: fused-optimizer group");
     const int count = static_cast<int>(g->plans.size());
     bool fuse = true;
     for (int i = 0; i < count; ++i) {
@@ -1033,8 +1164,8 @@ tag_status_t tag_sfb_group_sync_sharded(tag_sfb_group_t g, const void* const* X,
 tag_status_t tag_sfb_group_sync(tag_sfb_group_t g, const void* const* X, const void* const* dY,
                                 void* const* dW, tag_stream_t stream) {
     if (!g || !X || !dY || !dW) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync: NULL argument");
-    if (g->plans[0]->d.fuse_sgd)
-        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync: fuse_sgd group, use sync_sgd");
+    if (g->plans[0]->d.fuse_sgd || g->plans[0]->d.fuse_adam)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_sync: fused-optimizer group, use sync_sgd / sync_adam");
     const int count = static_cast<int>(g->plans.size());
     bool fuse = true;
     for (int i = 0; i < count; ++i) {

@@ -10,6 +10,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include "optim.cuh"
 #include "tag_internal.h"
 
 namespace tag {
@@ -189,6 +190,34 @@ tag_status_t launch_tf32_split(const float* src, float* dst, int64_t K, int64_t 
     tf32_split_kernel<<<grid_for(kpad * cols), 256, 0, s>>>(src, dst, K, cols, kpad);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "launch tf32_split_kernel");
+    count_launch();
+    return TAG_OK;
+}
+
+namespace {
+__global__ void __launch_bounds__(256)
+adam_kernel(const float* __restrict__ dW, float* __restrict__ W, float* __restrict__ Mm,
+            float* __restrict__ V, int64_t len, AdamConsts c) {
+    const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = tid; i < len; i += nthreads) {
+        float w = W[i], m = Mm[i], v = V[i];
+        adam_update(dW[i], w, m, v, c);
+        W[i] = w;
+        Mm[i] = m;
+        V[i] = v;
+    }
+}
+}  // namespace
+
+tag_status_t launch_adam(const float* dW, float* W, float* Mm, float* V, int64_t len, float b1,
+                         float omb1, float b2, float omb2, float eps, float lr_t, float isbc2,
+                         float wd, cudaStream_t s) {
+    if (len == 0) return TAG_OK;
+    const AdamConsts c{b1, omb1, b2, omb2, eps, lr_t, isbc2, wd};
+    adam_kernel<<<grid_for(len), 256, 0, s>>>(dW, W, Mm, V, len, c);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "launch adam_kernel");
     count_launch();
     return TAG_OK;
 }

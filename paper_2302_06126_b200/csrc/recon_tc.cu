@@ -33,6 +33,7 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include "optim.cuh"
 #include "ptx.cuh"
 #include "tag_internal.h"
 
@@ -104,7 +105,8 @@ struct LayerParams {
     CUtensorMap tmB;  // dY_all (K x N)
     void* C;          // dW out (may be nullptr with SGD)
     float* W;
-    float* V;
+    float* V;         // SGD momentum buffer / Adam second moment
+    float* Mm;        // Adam first moment
     int M, N;
     int num_n_blocks, num_k_blocks;
     int k_lo;         // X3: first row of the lo halves (Kp)
@@ -126,6 +128,8 @@ struct GroupParams {
     int count;
     int num_tiles;
     float lr, mu, wd;
+    int opt;               // optimizer epilogue (SGD instantiations): 1 SGD-momentum, 2 Adam
+    AdamConsts adam;
     int slot;              // this rank (its slot in X_all / dY_all)
     char* mc_base;         // FUSED: NVLS multicast base of the windows, or nullptr (unicast)
     int dbg;               // TAG_FUSED_DEBUG (profiling only): 1 no push/wait, 2 no wait, 3 stamps
@@ -591,6 +595,44 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                         continue;
                     }
                     if constexpr (SGD) {
+                        if (full && gp.opt == 2) {
+                            // E3 Adam fast path: W, m, v of four rows in flight at a time
+                            float4* wp4 = reinterpret_cast<float4*>(Wp + off0);
+                            float4* mp4 = reinterpret_cast<float4*>(lp.Mm + off0);
+                            float4* vp4 = reinterpret_cast<float4*>(Vp + off0);
+                            const int64_t gstep = step / 4;
+#pragma unroll
+                            for (int hh = 0; hh < 2; ++hh) {
+                                float4 wv[4], mv[4], vv[4];
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const int r = 4 * hh + i;
+                                    wv[i] = __ldcs(wp4 + r * gstep);
+                                    mv[i] = __ldcs(mp4 + r * gstep);
+                                    vv[i] = __ldcs(vp4 + r * gstep);
+                                }
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const int r = 4 * hh + i;
+                                    uint32_t dw[4];
+                                    ptx::ld_shared_v4(sq + r * 512 + ((r & 1) ? sw1 : sw0), dw[0],
+                                                      dw[1], dw[2], dw[3]);
+                                    float* wf = reinterpret_cast<float*>(&wv[i]);
+                                    float* mf = reinterpret_cast<float*>(&mv[i]);
+                                    float* vf = reinterpret_cast<float*>(&vv[i]);
+#pragma unroll
+                                    for (int e = 0; e < 4; ++e)
+                                        adam_update(__uint_as_float(dw[e]), wf[e], mf[e], vf[e], gp.adam);
+                                    __stcs(wp4 + r * gstep, wv[i]);
+                                    __stcs(mp4 + r * gstep, mv[i]);
+                                    __stcs(vp4 + r * gstep, vv[i]);
+                                    if (Cp != nullptr)
+                                        __stcs(reinterpret_cast<uint4*>(Cp + (off0 + r * step) * ESZ),
+                                               make_uint4(dw[0], dw[1], dw[2], dw[3]));
+                                }
+                            }
+                            continue;
+                        }
                         if (full) {
                             // E2 fast path: all 16 loads of W and v in flight before any math
                             // (the per-row load -> update -> store chain would serialise on the
@@ -635,7 +677,6 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                         if (!col_ok || row0 + r >= M) continue;
                         const int64_t off = off0 + i * step;
                         if constexpr (SGD) {
-                            // E2 (R14): g = dW + wd*W ; v = mu*v + g ; W -= lr*v   (fp32)
                             float4* wp = reinterpret_cast<float4*>(Wp + off);
                             float4* vp = reinterpret_cast<float4*>(Vp + off);
                             float4 wv = __ldcs(wp);
@@ -644,11 +685,22 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                                                  __uint_as_float(c), __uint_as_float(d)};
                             float* wf = reinterpret_cast<float*>(&wv);
                             float* vf = reinterpret_cast<float*>(&vv);
+                            if (gp.opt == 2) {
+                                // E3 Adam (R22)
+                                float4* mp = reinterpret_cast<float4*>(lp.Mm + off);
+                                float4 mv = __ldcs(mp);
+                                float* mf = reinterpret_cast<float*>(&mv);
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) {
-                                const float g = __fadd_rn(dv[e], __fmul_rn(wd, wf[e]));
-                                vf[e] = __fadd_rn(__fmul_rn(mu, vf[e]), g);
-                                wf[e] = __fsub_rn(wf[e], __fmul_rn(lr, vf[e]));
+                                for (int e = 0; e < 4; ++e) adam_update(dv[e], wf[e], mf[e], vf[e], gp.adam);
+                                __stcs(mp, mv);
+                            } else {
+                                // E2 (R14): g = dW + wd*W ; v = mu*v + g ; W -= lr*v   (fp32)
+#pragma unroll
+                                for (int e = 0; e < 4; ++e) {
+                                    const float g = __fadd_rn(dv[e], __fmul_rn(wd, wf[e]));
+                                    vf[e] = __fadd_rn(__fmul_rn(mu, vf[e]), g);
+                                    wf[e] = __fsub_rn(wf[e], __fmul_rn(lr, vf[e]));
+                                }
                             }
                             __stcs(wp, wv);
                             __stcs(vp, vv);
@@ -759,6 +811,7 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
         L.C = a[i].C;
         L.W = a[i].W;
         L.V = a[i].V;
+        L.Mm = a[i].Mm;
         L.M = static_cast<int>(a[i].M);
         L.N = static_cast<int>(a[i].N);
         L.num_n_blocks = static_cast<int>((a[i].N + BN - 1) / BN);
@@ -788,6 +841,9 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     gp.lr = a[0].lr;
     gp.mu = a[0].mu;
     gp.wd = a[0].wd;
+    gp.opt = a[0].opt;
+    gp.adam = AdamConsts{a[0].b1, a[0].omb1, a[0].b2, a[0].omb2, a[0].eps, a[0].lr_t, a[0].isbc2,
+                         a[0].wd};
     gp.slot = FUSED ? fg->me : 0;
     gp.mc_base = FUSED ? static_cast<char*>(fg->mc_base) : nullptr;
     static const int dbg = [] {
@@ -866,6 +922,7 @@ bool recon_tc_ok(const ReconArgs& a) {
     if (a.C && reinterpret_cast<uintptr_t>(a.C) % 16) return false;
     if (a.sgd && (reinterpret_cast<uintptr_t>(a.W) % 16 || reinterpret_cast<uintptr_t>(a.V) % 16))
         return false;
+    if (a.sgd && a.opt == 2 && (a.Mm == nullptr || reinterpret_cast<uintptr_t>(a.Mm) % 16)) return false;
     return true;
 }
 
@@ -881,7 +938,8 @@ tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s
                                    const FusedGather* fused) {
     if (count < 1 || count > MAX_GROUP) return fail(TAG_ERR_INVALID_ARG, "recon group size");
     for (int i = 0; i < count; ++i)
-        if (a[i].sgd != a[0].sgd || a[i].out != a[0].out || a[i].wire != a[0].wire)
+        if (a[i].sgd != a[0].sgd || a[i].out != a[0].out || a[i].wire != a[0].wire ||
+            (a[i].sgd && a[i].opt != a[0].opt))
             return fail(TAG_ERR_INVALID_ARG, "recon group: mixed epilogues or operand dtypes");
     return fused ? dispatch<true>(a, count, s, fused) : dispatch<false>(a, count, s, nullptr);
 }

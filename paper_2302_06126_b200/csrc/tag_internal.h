@@ -40,6 +40,11 @@ struct ReconArgs {
     float* W;
     float* V;
     float lr, mu, wd;
+    // optimizer kind when sgd (= an optimizer epilogue) is set: 1 SGD-momentum, 2 Adam (R22);
+    // Adam keeps its first moment in Mm and its second in V
+    int opt;
+    float* Mm;
+    float b1, omb1, b2, omb2, eps, lr_t, isbc2;
     // fused NVLink all-gather (push of this rank's factors inside the reconstruction kernel)
     const void* srcX;      // X_r, dY_r (in dtype: wire dtype, or fp32 with FusedGather::cast)
     const void* srcY;
@@ -108,6 +113,12 @@ tag_status_t launch_bias_grad(const BiasArgs* a, int count, cudaStream_t s);
 tag_status_t launch_tf32_split(const float* src, float* dst, int64_t K, int64_t cols, int64_t kpad,
                                cudaStream_t s);
 constexpr int TF32_KALIGN = 16;   // kpad = K rounded up to the 3xTF32 stage depth
+
+// ------------------------------------------------------------------ unfused Adam (R22)
+// W, m, v updated in place from dW (all fp32, len elements); constants as in optim.cuh
+tag_status_t launch_adam(const float* dW, float* W, float* Mm, float* V, int64_t len, float b1,
+                         float omb1, float b2, float omb2, float eps, float lr_t, float isbc2,
+                         float wd, cudaStream_t s);
 
 // ------------------------------------------------------------------ unfused SGD
 tag_status_t launch_sgd(const float* dW, float* W, float* V, int64_t len, float lr, float mu,

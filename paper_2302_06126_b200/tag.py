@@ -34,7 +34,9 @@ class SfbDesc(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int64), ("N", ctypes.c_int64), ("B", ctypes.c_int64),
                 ("n", ctypes.c_int), ("in_dtype", ctypes.c_int), ("wire_dtype", ctypes.c_int),
                 ("out_dtype", ctypes.c_int), ("fuse_sgd", ctypes.c_int), ("lr", ctypes.c_float),
-                ("momentum", ctypes.c_float), ("weight_decay", ctypes.c_float)]
+                ("momentum", ctypes.c_float), ("weight_decay", ctypes.c_float),
+                ("fuse_adam", ctypes.c_int), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
+                ("eps", ctypes.c_float)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -93,6 +95,7 @@ _SIGS = {
     "tag_sfb_reconstruct": ([_vp, _vp, _vp], _st),
     "tag_sfb_bias_grad": ([_vp, _vp, _vp], _st),
     "tag_sfb_sync_sgd": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], _st),
+    "tag_sfb_sync_adam": ([_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp, _vp], _st),
     "tag_sfb_sync_host": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_shard_rows": ([_vp, _i, _p(ctypes.c_int64), _p(ctypes.c_int64)], _st),
     "tag_sfb_sync_sharded": ([_vp, _vp, _vp, _vp, _vp], _st),
@@ -100,6 +103,7 @@ _SIGS = {
     "tag_dense_allreduce": ([_vp, _vp, _vp], _st),
     "tag_ps_sync": ([_vp, _vp, _i, _vp], _st),
     "tag_sgd_step": ([_vp, _vp, _vp, _vp, _vp], _st),
+    "tag_adam_step": ([_vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp], _st),
     "tag_sfb_select": ([_p(LayerDesc), _i, _p(Topology), _p(_i)], _st),
     "tag_sfb_select_profiled": ([_p(LayerDesc), _i, _p(ProfiledTopology), _p(_i)], _st),
     "tag_sfb_ilp_solve": ([_p(IlpInstance), _p(ctypes.c_uint8), _p(ctypes.c_double)], _st),
@@ -109,6 +113,8 @@ _SIGS = {
     "tag_sfb_group_sync": ([_vp, _p(_vp), _p(_vp), _p(_vp), _vp], _st),
     "tag_sfb_group_gather": ([_vp, _p(_vp), _p(_vp), _vp], _st),
     "tag_sfb_group_sync_sgd": ([_vp, _p(_vp), _p(_vp), _p(_vp), _p(_vp), _p(_vp), _vp], _st),
+    "tag_sfb_group_sync_adam": ([_vp, _p(_vp), _p(_vp), _p(_vp), _p(_vp), _p(_vp), ctypes.c_int64,
+                                 _p(_vp), _vp], _st),
     "tag_sfb_group_reconstruct": ([_vp, _p(_vp), _vp], _st),
     "tag_sfb_group_bias_grad": ([_vp, _p(_vp), _vp], _st),
 }
@@ -204,13 +210,15 @@ class SfbPlan:
     """One replicated Dense layer W (M x N), B rows per replica, n replicas (= comm size)."""
 
     def __init__(self, comm, M, N, B, in_dtype="bf16", wire_dtype="bf16", out_dtype="f32",
-                 fuse_sgd=False, lr=0.0, momentum=0.0, weight_decay=0.0):
+                 fuse_sgd=False, lr=0.0, momentum=0.0, weight_decay=0.0, fuse_adam=False,
+                 beta1=0.9, beta2=0.999, eps=1e-8):
         self.comm = comm
         self.M, self.N, self.B, self.n = M, N, B, comm.nranks
         self.in_dtype, self.wire_dtype, self.out_dtype = (_DT_OF[in_dtype], _DT_OF[wire_dtype],
                                                           _DT_OF[out_dtype])
         d = SfbDesc(M, N, B, comm.nranks, self.in_dtype, self.wire_dtype, self.out_dtype,
-                    1 if fuse_sgd else 0, lr, momentum, weight_decay)
+                    1 if fuse_sgd else 0, lr, momentum, weight_decay, 1 if fuse_adam else 0,
+                    beta1, beta2, eps)
         h = _vp()
         _check(_lib.tag_sfb_plan(comm.handle, ctypes.byref(d), ctypes.byref(h)), "tag_sfb_plan")
         self._h = h
@@ -262,6 +270,23 @@ class SfbPlan:
         _check(_lib.tag_sfb_sync_sgd(self._h, x, dy, _dev(W, torch.float32, shape, "W"),
                                      _dev(v, torch.float32, shape, "v"), dw, _stream(stream)),
                "tag_sfb_sync_sgd")
+
+    def sync_adam(self, X, dY, W, m, v, step, dW=None, stream=None):
+        """tag_sfb_sync with Adam fused into the epilogue (step >= 1)."""
+        x, dy = self._xy(X, dY)
+        shape = (self.M, self.N)
+        dw = _dev(dW, self.out_torch, shape, "dW") if dW is not None else _vp()
+        _check(_lib.tag_sfb_sync_adam(self._h, x, dy, _dev(W, torch.float32, shape, "W"),
+                                      _dev(m, torch.float32, shape, "m"),
+                                      _dev(v, torch.float32, shape, "v"), step, dw,
+                                      _stream(stream)), "tag_sfb_sync_adam")
+
+    def adam_step(self, dW, W, m, v, step, stream=None):
+        shape = (self.M, self.N)
+        _check(_lib.tag_adam_step(self._h, _dev(dW, torch.float32, shape, "dW"),
+                                  _dev(W, torch.float32, shape, "W"), _dev(m, torch.float32, shape, "m"),
+                                  _dev(v, torch.float32, shape, "v"), step, _stream(stream)),
+               "tag_adam_step")
 
     def shard_rows(self, rank=None):
         """(row_begin, row_count) of `rank`'s dW shard (default: this rank)."""
@@ -359,6 +384,15 @@ class SfbGroup:
         dW = self._ptrs(dWs, "dW") if dWs is not None else None
         _check(_lib.tag_sfb_group_sync_sgd(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"), W,
                                            v, dW, _stream(stream)), "tag_sfb_group_sync_sgd")
+
+    def sync_adam(self, Xs, dYs, Ws, ms, vs, step, dWs=None, stream=None):
+        shapes = [(p.M, p.N) for p in self.plans]
+        arr = lambda ts, nm: (_vp * len(self.plans))(*[_dev(t, torch.float32, s_, nm)   # noqa: E731
+                                                      for t, s_ in zip(ts, shapes)])
+        dW = self._ptrs(dWs, "dW") if dWs is not None else None
+        _check(_lib.tag_sfb_group_sync_adam(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"),
+                                            arr(Ws, "W"), arr(ms, "m"), arr(vs, "v"), step, dW,
+                                            _stream(stream)), "tag_sfb_group_sync_adam")
 
     def gather(self, Xs, dYs, stream=None):
         _check(_lib.tag_sfb_group_gather(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"),

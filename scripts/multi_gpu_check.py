@@ -10,7 +10,7 @@ gradients"):
   3. random VGG-shaped inputs: rel. Frobenius <= 1e-5 vs the oracle on the exact bf16 values;
   4. the dense baseline (local GEMM + AllReduce with PreMulSum 1/(nB)) agrees with SFB;
   5. fp32 toy config (64x32, B=4) <= 1e-5; fp32 -> bf16 wire (pack + in-place gather);
-  6. fused SGD-momentum: identical W, v on every rank and equal to the unfused path;
+  6. fused SGD-momentum: identical W, v on every rank and equal to the unfused path (6b: Adam);
   7. selector decisions identical on every rank and equal to the oracle's;
   11. the bias gradient from the gathered dY_all: bit-exact on integers, identical on all ranks;
   12. Replicate-with-PS (reduce to a round-robin PS + broadcast) equals the dense route;
@@ -137,6 +137,26 @@ def main():
     torch.cuda.synchronize()
     hashes = tdist.all_gather_object(digest(W1) + digest(v1))
     record("fused_sgd", torch.equal(W1, W2) and torch.equal(v1, v2) and len(set(hashes)) == 1)
+    plan.close()
+
+    # 6b: fused Adam (R22) at n > 1 == sync + unfused Adam, identical on every rank
+    M, N, B = 4096, 1024, 32
+    X, dY = synth.factors(5, 4, rank, M, N, B, "normal", "small")
+    W0, _ = synth.sgd_state(5, 4, M, N)
+    plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", fuse_adam=True, lr=1e-3,
+                       weight_decay=0.01)
+    Xd, dYd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(dY).to(torch.bfloat16).cuda()
+    W1, m1, v1 = torch.from_numpy(W0).cuda(), torch.zeros(M, N, device="cuda"), torch.zeros(M, N, device="cuda")
+    W2, m2, v2 = W1.clone(), m1.clone(), v1.clone()
+    dW2 = torch.empty(M, N, device="cuda")
+    for t in (1, 2, 3):
+        plan.sync_adam(Xd, dYd, W1, m1, v1, t)
+        plan.sync(Xd, dYd, dW2)
+        plan.adam_step(dW2, W2, m2, v2, t)
+    torch.cuda.synchronize()
+    hashes = tdist.all_gather_object(digest(W1) + digest(m1) + digest(v1))
+    record("fused_adam", torch.equal(W1, W2) and torch.equal(m1, m2) and torch.equal(v1, v2)
+           and len(set(hashes)) == 1)
     plan.close()
 
     # 8: a bucket (one push kernel + one reconstruction launch) == per-layer syncs, bit for bit

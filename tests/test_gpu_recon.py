@@ -476,3 +476,99 @@ def test_fp32_wire_sgd_fused(tag, comm1, oracle_mod):
     torch.cuda.synchronize()
     p.close()
     assert torch.equal(W1, W2) and torch.equal(v1, v2)
+
+
+# ------------------------------------------------------------------ Adam epilogue (R22)
+ADAM_HP = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+
+
+@pytest.mark.parametrize("M,N,K,wire", [(4096, 1000, 32, "bf16"), (1024, 4096, 128, "bf16"),
+                                         (4096, 4096, 256, "bf16"), (512, 1024, 32, "f32"),
+                                         (130, 257, 10, "bf16"), (136, 264, 40, "bf16")])
+def test_adam_fused_equals_unfused(tag, comm1, M, N, K, wire):
+    """E3 (tensor-core epilogue; SIMT shapes: reconstruction + unfused kernel) == tag_sfb_sync
+    followed by tag_adam_step, bit for bit, over three steps (one CTA, CTA pairs, 3xTF32)."""
+    rs = np.random.default_rng(73)
+    dt = TORCH[wire]
+    X = torch.from_numpy(rs.standard_normal((K, M)).astype(np.float32)).to(dt).cuda()
+    dY = torch.from_numpy(rs.standard_normal((K, N)).astype(np.float32)).to(dt).cuda()
+    W0 = torch.from_numpy((0.02 * rs.standard_normal((M, N))).astype(np.float32)).cuda()
+    p = tag.SfbPlan(comm1, M, N, K, wire, wire, "f32", fuse_adam=True, **ADAM_HP)
+    W1, m1, v1 = W0.clone(), torch.zeros_like(W0), torch.zeros_like(W0)
+    W2, m2, v2 = W0.clone(), torch.zeros_like(W0), torch.zeros_like(W0)
+    dW = torch.empty_like(W0)
+    for t in (1, 2, 3):
+        p.sync_adam(X, dY, W1, m1, v1, t)
+        p.sync(X, dY, dW)
+        p.adam_step(dW, W2, m2, v2, t)
+    torch.cuda.synchronize()
+    p.close()
+    assert torch.equal(W1, W2) and torch.equal(m1, m2) and torch.equal(v1, v2)
+    assert not torch.equal(W1, W0)
+
+
+def test_adam_matches_oracle(tag, comm1, oracle_mod):
+    """Two fused Adam steps vs the fp64 oracle (reconstruction from the exact bf16 operands, then
+    torch.optim.Adam-semantics updates): the weight change agrees to 1e-4 relative."""
+    rs = np.random.default_rng(74)
+    K, M, N = 64, 520, 1000
+    X = rs.standard_normal((K, M)).astype(np.float32)
+    dY = rs.standard_normal((K, N)).astype(np.float32)
+    W0 = (0.02 * rs.standard_normal((M, N))).astype(np.float32)
+    p = tag.SfbPlan(comm1, M, N, K, "bf16", "bf16", "f32", fuse_adam=True, **ADAM_HP)
+    W, m, v = torch.from_numpy(W0).cuda(), torch.zeros((M, N), device="cuda"), torch.zeros((M, N), device="cuda")
+    for t in (1, 2):
+        p.sync_adam(to_dev(X, "bf16"), to_dev(dY, "bf16"), W, m, v, t)
+    torch.cuda.synchronize()
+    p.close()
+    dW = oracle_mod.sfb_dw(exact_values(X, "bf16")[None], exact_values(dY, "bf16")[None])
+    Wr, mr, vr = W0.astype(np.float64), np.zeros((M, N)), np.zeros((M, N))
+    # the plan holds its hyper-parameters as fp32 (tag_sfb_desc_t): fl32(0.999) makes 1 - beta2
+    # differ from 0.001 by 1.3e-5 relative, so the oracle is given the same fp32 values
+    hp32 = {k: float(np.float32(v)) for k, v in ADAM_HP.items()}
+    for t in (1, 2):
+        Wr, mr, vr = oracle_mod.adam(dW, Wr, mr, vr, hp32["lr"], hp32["beta1"], hp32["beta2"],
+                                     hp32["eps"], hp32["weight_decay"], t)
+    assert rel_fro(W.cpu().numpy() - W0, Wr - W0) <= 1e-4
+    assert rel_fro(m.cpu().numpy(), mr) <= 1e-5 and rel_fro(v.cpu().numpy(), vr) <= 1e-5
+
+
+def test_group_adam_equals_per_plan(tag, comm1):
+    rs = np.random.default_rng(75)
+    layers = [(4096, 1000, 32), (1024, 4096, 32), (512, 2048, 32)]
+    plans, Xs, dYs, Ws, ms, vs, W2, m2, v2 = [], [], [], [], [], [], [], [], []
+    for M, N, K in layers:
+        plans.append(tag.SfbPlan(comm1, M, N, K, fuse_adam=True, **ADAM_HP))
+        Xs.append(torch.from_numpy(rs.standard_normal((K, M))).to(torch.bfloat16).cuda())
+        dYs.append(torch.from_numpy(rs.standard_normal((K, N))).to(torch.bfloat16).cuda())
+        w = torch.from_numpy((0.02 * rs.standard_normal((M, N))).astype(np.float32)).cuda()
+        Ws.append(w.clone()); W2.append(w.clone())
+        ms.append(torch.zeros_like(w)); m2.append(torch.zeros_like(w))
+        vs.append(torch.zeros_like(w)); v2.append(torch.zeros_like(w))
+    g = tag.SfbGroup(plans)
+    for t in (1, 2):
+        g.sync_adam(Xs, dYs, Ws, ms, vs, t)
+        for i, p in enumerate(plans):
+            p.sync_adam(Xs[i], dYs[i], W2[i], m2[i], v2[i], t)
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(Ws + ms + vs, W2 + m2 + v2))
+    g.close()
+    for p in plans:
+        p.close()
+
+
+def test_adam_validation(tag, comm1):
+    with pytest.raises(tag.TagError):
+        tag.SfbPlan(comm1, 64, 32, 8, fuse_adam=True, fuse_sgd=True, lr=1e-3)
+    with pytest.raises(tag.TagError):
+        tag.SfbPlan(comm1, 64, 32, 8, fuse_adam=True, lr=1e-3, beta1=1.0)
+    with pytest.raises(tag.TagError):
+        tag.SfbPlan(comm1, 64, 32, 8, "bf16", "bf16", "bf16", fuse_adam=True, lr=1e-3)
+    p = tag.SfbPlan(comm1, 64, 32, 8, fuse_adam=True, lr=1e-3)
+    X, dY = torch.zeros((8, 64), dtype=torch.bfloat16, device="cuda"), torch.zeros((8, 32), dtype=torch.bfloat16, device="cuda")
+    W, m, v = (torch.zeros((64, 32), device="cuda") for _ in range(3))
+    with pytest.raises(tag.TagError):
+        p.sync_adam(X, dY, W, m, v, 0)                      # step must be >= 1
+    with pytest.raises(tag.TagError):
+        p.sync_sgd(X, dY, W, v)                             # not an SGD plan
+    p.close()
