@@ -401,7 +401,9 @@ def main():
     launches0 = tag.kernel_launches()
     with ClockSampler(local_rank) as clk:
         steps_ms = timed_steps(args.steps)
-    launches = tag.kernel_launches() - launches0
+    # libtag kernels inside the timed intervals: the per-step pre-start barrier kernel (n > 1) is
+    # launched before each start event, so it is counted by the library but not timed
+    launches = tag.kernel_launches() - launches0 - (args.steps if n > 1 else 0)
     torch.cuda.synchronize()
     tdist.barrier()
     nstaged = max(5, min(args.steps, 30))
