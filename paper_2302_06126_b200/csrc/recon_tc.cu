@@ -41,11 +41,20 @@ namespace tag {
 namespace {
 
 constexpr int BM = 128;                  // UMMA M (TMEM lanes)
-constexpr int NUM_EPI_WARPS = 8;
+#ifndef EXP_EPI_WARPS
+#define EXP_EPI_WARPS 8
+#endif
+constexpr int NUM_EPI_WARPS = EXP_EPI_WARPS;
+constexpr int EPI_GROUPS = NUM_EPI_WARPS / 4;   // column groups per TMEM lane quadrant
 constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;   // 320
 constexpr int EPI_CHUNK_BYTES = 32 * 128;    // one 32 rows x 128 B transpose buffer
 constexpr int SMEM_MAX = 232448;              // 227 KB of dynamic shared memory per CTA
 constexpr int TMEM_COLS = 512;
+// Diagnostics only (scripts/build_variant.sh, never the product build): 1 = epilogue skips the
+// global stores, 2 = epilogue releases each accumulator without reading it
+#ifndef EXP_EPI_MODE
+#define EXP_EPI_MODE 0
+#endif
 
 // CTAS = 2: a CTA pair on one TPC runs tcgen05 cta_group::2 — UMMA M = 256 (128 rows of A in
 // each CTA's smem), N = BN (BN/2 columns of B in each CTA's smem), each CTA's TMEM holds its
@@ -113,6 +122,7 @@ struct LayerParams {
     int tile_begin;   // first global tile index of this layer
     int num_m_blocks;
     int m_fast;       // 1: consecutive tiles walk down M (share a B panel), else along N
+    int box3;         // 1: tmA / tmB are 3-D maps (64 x BK x chunks): one request per operand
     float alpha;
     // fused all-gather (FUSED = true): this rank's factors are pushed into every peer's window
     const void* srcX;      // X_r (B x M, wire dtype)
@@ -371,6 +381,13 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                         const uint32_t fbl = ptx::mapa(fb, 0);
                         if (crank == 0) ptx::mbar_arrive_expect_tx(fb, CTAS * C::STAGE_BYTES);
                         else ptx::mbar_arrive_cluster(fbl);
+                        if (gp.L[tr.li].box3) {
+                            // all MN chunks of an operand in one 3-D request (16 KB each)
+                            ptx::tma_load_3d_cg2(sa, tmA, fbl, 0, kb * C::BK, am0 / C::ELEMS);
+                            ptx::tma_load_3d_cg2(sb, tmB, fbl, 0, kb * C::BK, bn0 / C::ELEMS);
+                            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                            continue;
+                        }
 #pragma unroll
                         for (int c = 0; c < C::A_CHUNKS; ++c)
                             ptx::tma_load_2d_cg2(sa + c * C::CHUNK_BYTES, tmA, fbl, am0 + C::ELEMS * c, kb * C::BK);
@@ -455,11 +472,13 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
         // 32-B sectors but 8 lines per instruction — write HBM ~15 % slower at K = 32.)
         const int ew = warp - 2;                 // 0..7
         const int quad = warp & 3;               // TMEM lane quadrant this warp may access
-        const int half = ew >> 2;                // which half of the tile's columns
+        const int half = ew >> 2;                // which column group of the tile
+        constexpr int GC = BN / EPI_GROUPS;      // columns per group
         const uint32_t sbuf = s_epi + ew * C::EPI_BUF_BYTES;
         constexpr int ESZ = OUT_BF16 ? 2 : 4;
         constexpr int COLS_PER_CHUNK = 128 / ESZ;               // 128 bytes of output per row
-        constexpr int CHUNKS = (BN / 2) / COLS_PER_CHUNK;
+        constexpr int CHUNKS = GC / COLS_PER_CHUNK;
+        static_assert(CHUNKS >= 1, "epilogue column group narrower than one 128-byte chunk");
         constexpr int VEC = 16 / ESZ;                           // output elements per 16 B
         constexpr int PAIR = EP;                                // chunks staged per round
         const int sub = lane >> 3;               // row within a 4-row group (write-out phase)
@@ -483,8 +502,9 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
             ptx::tc_fence_after();
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quad) << 16) + acc * C::ACC_COLS;
             // chunks of this warp's column half that hold any output column (warp-uniform)
-            int nch = (N - (n0 + half * (BN / 2)) + COLS_PER_CHUNK - 1) / COLS_PER_CHUNK;
+            int nch = (N - (n0 + half * GC) + COLS_PER_CHUNK - 1) / COLS_PER_CHUNK;
             nch = nch < 0 ? 0 : (nch > CHUNKS ? CHUNKS : nch);
+            if (EXP_EPI_MODE == 2) nch = 0;
             if (nch == 0) {                       // nothing to read: release the accumulator
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -501,7 +521,7 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
 #pragma unroll
                 for (int q = 0; q < PAIR; ++q) {
                     if (q >= np) break;
-                    const uint32_t tc = t_row + half * (BN / 2) + (ch + q) * COLS_PER_CHUNK;
+                    const uint32_t tc = t_row + half * GC + (ch + q) * COLS_PER_CHUNK;
                     if constexpr (OUT_BF16) {
                         uint32_t r0[32], r1[32];
                         ptx::tmem_ld_32x32b_x32(tc, r0);
@@ -535,7 +555,7 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                     ptx::tmem_wait_ld();
                     if constexpr (X3) {           // + the lo accumulator (PAIR = 1), one fp32 add
                         uint32_t l[32];
-                        ptx::tmem_ld_32x32b_x32(t_row + half * (BN / 2) + ch * COLS_PER_CHUNK + BN, l);
+                        ptx::tmem_ld_32x32b_x32(t_row + half * GC + ch * COLS_PER_CHUNK + BN, l);
                         ptx::tmem_wait_ld();
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
@@ -556,6 +576,28 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                     else ptx::mbar_arrive(bar_tempty + 8 * acc);
                 }
                 }
+                if constexpr (EXP_EPI_MODE == 3 || EXP_EPI_MODE == 4) {
+                    // diagnostics: 3 = direct 16-B stores of each lane's row segment (no smem),
+                    // 4 = TMEM read only
+#pragma unroll
+                    for (int q = 0; q < PAIR; ++q) {
+                        if (q >= np) break;
+                        const int gc = n0 + half * GC + (ch + q) * COLS_PER_CHUNK;
+                        const int r = row0 + static_cast<int>(lane);
+                        if (EXP_EPI_MODE == 4) {
+                            uint32_t x = 0;
+                            for (int i = 0; i < 32; ++i) x ^= w[q][i];
+                            if (x == 0x7f7f7f7fu && r < 0) Cp[0] = 1;
+                            continue;
+                        }
+                        if (r >= M || gc + COLS_PER_CHUNK > N) continue;
+                        uint4* g = reinterpret_cast<uint4*>(Cp + (static_cast<int64_t>(r) * N + gc) * ESZ);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j)
+                            __stcs(g + j, make_uint4(w[q][4 * j], w[q][4 * j + 1], w[q][4 * j + 2], w[q][4 * j + 3]));
+                    }
+                    continue;
+                }
                 // ---- registers -> 128B-swizzled smem (row `lane`), conflict-free
                 __syncwarp();                     // previous round's smem reads are done
 #pragma unroll
@@ -572,15 +614,25 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
 #pragma unroll
                 for (int q = 0; q < PAIR; ++q) {
                     if (q >= np) break;
-                    const int gcol = n0 + half * (BN / 2) + (ch + q) * COLS_PER_CHUNK + cj * VEC;
+                    const int gcol = n0 + half * GC + (ch + q) * COLS_PER_CHUNK + cj * VEC;
                     const bool col_ok = gcol < N;   // N % 8 == 0: a 16-B slot is all in or out
                     const int64_t off0 = static_cast<int64_t>(row0 + sub) * N + gcol;
                     const int64_t step = 4 * static_cast<int64_t>(N);
                     // warp-uniform: every row and column of this 32 x 128-B chunk is in range
                     const bool full = row0 + 32 <= M &&
-                                      n0 + half * (BN / 2) + (ch + q + 1) * COLS_PER_CHUNK <= N;
+                                      n0 + half * GC + (ch + q + 1) * COLS_PER_CHUNK <= N;
                     const uint32_t sq = sbuf + q * 4096 + sub * 128;
                     const uint32_t sw0 = (cj ^ sub) << 4, sw1 = (cj ^ (sub + 4)) << 4;
+                    if (EXP_EPI_MODE == 1 && full && !SGD) {
+                        uint32_t a, b, c, d, x = 0;
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            ptx::ld_shared_v4(sq + i * 512 + ((i & 1) ? sw1 : sw0), a, b, c, d);
+                            x ^= a ^ b ^ c ^ d;
+                        }
+                        if (x == 0x7f7f7f7fu && row0 < 0) Cp[0] = 1;   // keep the loads
+                        continue;
+                    }
                     if (full && !SGD) {
                         // fast path (all but the edge tiles): no per-store predicates, the global
                         // address advances by 4 rows per store
@@ -754,6 +806,23 @@ bool encode_2d(CUtensorMap* m, const void* ptr, CUtensorMapDataType dt, int esiz
     return r == CUDA_SUCCESS;
 }
 
+// The same operand as a 3-D map {64 elements, rows, cols / 64 chunks} with a 128-byte chunk
+// stride: one box of `chunks` chunks x box_rows rows lands as consecutive 128-B-swizzled chunks,
+// exactly the 2-D layout, in one request. Needs cols % 64 == 0 (no chunk straddles a row end).
+bool encode_3d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_rows,
+               int chunks, int64_t ld = 0) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols / 64)};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>((ld ? ld : cols) * 2), 128};
+    cuuint32_t box[3] = {64, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(chunks)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 int tiles_for(const ReconArgs* a, int count, int bn, int ctas) {
     int64_t tiles = 0;
     for (int i = 0; i < count; ++i)
@@ -804,9 +873,20 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
         const int oes = X3 ? 4 : 2;
         const int64_t orows = X3 ? 2 * a[i].kpad : a[i].K;      // X3: [hi ; lo], Kp rows each
         const CUtensorMapSwizzle oswz = X3 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
-        if (!encode_2d(&L.tmA, a[i].A, odt, oes, orows, a[i].M, C::ELEMS, C::BK, a[i].lda, oswz) ||
-            !encode_2d(&L.tmB, a[i].Bm, odt, oes, orows, a[i].N, C::ELEMS, C::BK, 0, oswz))
+        static const bool no3 = [] {                                         // experiments
+            const char* e = std::getenv("TAG_RECON_NO3D");
+            return e != nullptr && *e != 0;
+        }();
+        L.box3 = CTAS == 2 && !X3 && !no3 && a[i].M % 64 == 0 && a[i].N % 64 == 0 &&
+                 a[i].lda % 64 == 0 ? 1 : 0;
+        if (L.box3) {
+            if (!encode_3d(&L.tmA, a[i].A, orows, a[i].M, C::BK, C::A_CHUNKS, a[i].lda) ||
+                !encode_3d(&L.tmB, a[i].Bm, orows, a[i].N, C::BK, C::B_CHUNKS))
+                return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed for the factor operands");
+        } else if (!encode_2d(&L.tmA, a[i].A, odt, oes, orows, a[i].M, C::ELEMS, C::BK, a[i].lda, oswz) ||
+                   !encode_2d(&L.tmB, a[i].Bm, odt, oes, orows, a[i].N, C::ELEMS, C::BK, 0, oswz)) {
             return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
+        }
         L.k_lo = X3 ? static_cast<int>(a[i].kpad) : 0;
         L.C = a[i].C;
         L.W = a[i].W;
