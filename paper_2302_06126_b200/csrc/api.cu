@@ -663,6 +663,16 @@ tag_status_t tag_sfb_plan_info(tag_sfb_plan_t p, tag_plan_info_t* out) {
     out->K = p->K;
     out->alpha = p->alpha;
     out->multicast = (p->gather_mode == TAG_GATHER_NVLINK_PUSH && p->comm->mc_base) ? 1 : 0;
+    out->recon_bn = out->recon_ctas = out->recon_box3d = 0;
+    if (p->use_tc) {
+        ReconArgs a{};
+        a.M = p->d.M;
+        a.N = p->d.N;
+        a.K = p->K;
+        a.wire = p->d.wire_dtype;
+        a.out = p->d.out_dtype;
+        recon_tc_describe(&a, 1, &out->recon_bn, &out->recon_ctas, &out->recon_box3d);
+    }
     return TAG_OK;
 }
 

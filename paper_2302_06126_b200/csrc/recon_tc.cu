@@ -1006,6 +1006,22 @@ bool recon_tc_ok(const ReconArgs& a) {
     return true;
 }
 
+void recon_tc_describe(const ReconArgs* a, int count, int* bn, int* ctas, int* box3d) {
+    if (a[0].wire == TAG_F32) {                  // 3xTF32: 128 x 128 single-CTA tiles
+        *bn = 128, *ctas = 1, *box3d = 0;
+        return;
+    }
+    const bool wide = big_tiles(a, count);
+    *bn = wide ? 256 : 128;
+    *ctas = wide ? use_ctas(a, count) : 1;
+    *box3d = 0;
+    if (*ctas == 2) {
+        const char* e = std::getenv("TAG_RECON_NO3D");
+        const bool no3 = e != nullptr && *e != 0;
+        *box3d = !no3 && a[0].M % 64 == 0 && a[0].N % 64 == 0 && a[0].lda % 64 == 0 ? 1 : 0;
+    }
+}
+
 int recon_tc_grid(const ReconArgs* a, int count) {
     const bool wide = big_tiles(a, count);
     const int ctas = wide ? use_ctas(a, count) : 1;

@@ -75,6 +75,8 @@ constexpr int MAX_GROUP = 8;
 tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s,
                                    const FusedGather* fused = nullptr);
 int recon_tc_grid(const ReconArgs* a, int count);
+// the tile configuration launch_recon_tc_group picks for these layers
+void recon_tc_describe(const ReconArgs* a, int count, int* bn, int* ctas, int* box3d);
 // SIMT FFMA path: any shape, fp32 or bf16 operands (exact fp32 accumulation in k order).
 tag_status_t launch_recon_simt(const ReconArgs& a, cudaStream_t s);
 

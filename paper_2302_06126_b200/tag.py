@@ -41,7 +41,9 @@ class SfbDesc(ctypes.Structure):
 
 class PlanInfo(ctypes.Structure):
     _fields_ = [("tensor_cores", ctypes.c_int), ("gather_mode", ctypes.c_int),
-                ("K", ctypes.c_int64), ("alpha", ctypes.c_float), ("multicast", ctypes.c_int)]
+                ("K", ctypes.c_int64), ("alpha", ctypes.c_float), ("multicast", ctypes.c_int),
+                ("recon_bn", ctypes.c_int), ("recon_ctas", ctypes.c_int),
+                ("recon_box3d", ctypes.c_int)]
 
 
 GATHER_NONE, GATHER_NCCL, GATHER_NVLINK_PUSH = 0, 1, 2
@@ -227,7 +229,9 @@ class SfbPlan:
         i = PlanInfo()
         _check(_lib.tag_sfb_plan_info(self._h, ctypes.byref(i)), "tag_sfb_plan_info")
         return {"tensor_cores": bool(i.tensor_cores), "gather": GATHER_NAMES[i.gather_mode],
-                "K": int(i.K), "alpha": float(i.alpha), "multicast": bool(i.multicast)}
+                "K": int(i.K), "alpha": float(i.alpha), "multicast": bool(i.multicast),
+                "recon_bn": int(i.recon_bn), "recon_ctas": int(i.recon_ctas),
+                "recon_box3d": bool(i.recon_box3d)}
 
     # dtypes as torch dtypes
     @property

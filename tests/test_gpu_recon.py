@@ -81,6 +81,27 @@ def test_integer_inputs_bit_exact(tag, comm1, oracle_mod, M, N, K, out_dt):
         f"max |diff| {np.abs(dW - want).max()}"
 
 
+# CTA-pair shapes (>= 74 pair tiles, K >= 192): 3-D boxes with ragged n-block and K tails, and
+# 2-D boxes (M not a multiple of 64) with ragged M, N and K
+PAIR_SHAPES = [((4352, 2112, 264), True), ((4104, 2008, 200), False)]
+
+
+@pytest.mark.parametrize("shape,box3d", PAIR_SHAPES)
+@pytest.mark.parametrize("out_dt", ["f32", "bf16"])
+def test_pair_path_integer_bit_exact(tag, comm1, oracle_mod, shape, box3d, out_dt):
+    M, N, K = shape
+    plan = tag.SfbPlan(comm1, M, N, K, "bf16", "bf16", out_dt)
+    info = plan.info()
+    plan.close()
+    assert (info["recon_bn"], info["recon_ctas"], info["recon_box3d"]) == (256, 2, box3d), info
+    X = synth.draw("int3", K, M, synth.rng(51, M, N, 0))
+    dY = synth.draw("int3", K, N, synth.rng(51, M, N, 1))
+    dW = run_sync(tag, comm1, X, dY, "bf16", "bf16", out_dt).float().cpu().numpy()
+    want = expected_int(oracle_mod, X, dY, K, out_dt)
+    assert np.array_equal(dW.view(np.uint32), want.view(np.uint32)), \
+        f"max |diff| {np.abs(dW - want).max()}"
+
+
 @pytest.mark.parametrize("n,B", [(1, 32), (2, 32), (4, 32), (8, 32), (8, 64)])
 def test_virtual_n_random_vgg_fc7(tag, comm1, oracle_mod, n, B):
     """VGG-19 fc7 shape (4096 x 4096) at K = n*B: post-ReLU X, masked small dY (d-2 recipe)."""
