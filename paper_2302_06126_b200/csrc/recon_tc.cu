@@ -358,10 +358,12 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                 if constexpr (FUSED) {
                     if (!(ready & (1u << tr.li))) {
                         if (gp.dbg == 0 || gp.dbg == 3) fused_wait(gp.L[tr.li], me);
+#ifdef TAG_FUSED_STAMPS   // profiling builds only: a printf in the kernel costs 1-2 us per launch
                         if (gp.dbg == 3 && ready == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
                             printf("fused rank %d cta %d push %llu ns, wait-after-push %llu ns\n", me,
                                    blockIdx.x, (unsigned long long)(t_pushed - t_start),
                                    (unsigned long long)(gtimer() - t_pushed));
+#endif
                         ready |= 1u << tr.li;
                     }
                 }

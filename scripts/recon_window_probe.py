@@ -1,7 +1,7 @@
 #!/usr/bin/env python3
-"""Fused push+reconstruction timing probe (torchrun): the VGG-19 bucket, cold (L2 flushed, ranks
-aligned by tag_comm_barrier), CUDA events around one tag_sfb_group_sync. TAG_FUSED_DEBUG=1/2/3
-select the profiling variants of the fused kernel (no push / no wait / printf stamps)."""
+"""Reconstruction-only time of the VGG-19 bucket at n = world size (torchrun), after an untimed
+gather, clean L2: does the operand buffer (NCCL symmetric window in push mode, cudaMalloc in
+TAG_GATHER=nccl mode) change the reconstruction's speed?"""
 import json
 import os
 import statistics
@@ -18,35 +18,30 @@ torch.cuda.set_device(local_rank)
 comm = tdist.bootstrap_comm(tag, local_rank)
 cfg = synth.CONFIGS[2]
 plans, Xs, dYs, dWs = [], [], [], []
-for li, L in enumerate(cfg.layers):
+for L in cfg.layers:
     plans.append(tag.SfbPlan(comm, L.M, L.N, L.B))
     Xs.append(torch.randn(L.B, L.M, device="cuda").to(torch.bfloat16))
     dYs.append(torch.randn(L.B, L.N, device="cuda").to(torch.bfloat16))
     dWs.append(torch.empty(L.M, L.N, device="cuda"))
 g = tag.SfbGroup(plans)
 flush = torch.empty(64 * 1024 * 1024, device="cuda")
-s = torch.cuda.Stream()
 ts = []
-iters = int(os.environ.get("ITERS", "20"))
-for it in range(iters + 3):
+for it in range(23):
+    g.gather(Xs, dYs)
     flush.zero_()
-    flush.sum()            # leave L2 holding clean lines (no write-back inside the timing)
+    flush.sum()
     torch.cuda.synchronize()
-    tdist.barrier()
-    with torch.cuda.stream(s):
-        torch.cuda._sleep(1_000_000)
-        comm.barrier(s)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        g.sync(Xs, dYs, dWs, s)
-        e1.record(s)
+    torch.cuda._sleep(1_000_000)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.reconstruct(dWs)
+    e1.record()
     torch.cuda.synchronize()
     if it >= 3:
         ts.append(e0.elapsed_time(e1))
 t = tdist.max_over_ranks(statistics.median(ts))
 if rank == 0:
-    print(json.dumps({"n": world, "dbg": os.environ.get("TAG_FUSED_DEBUG", "0"),
-                      "no_fuse": bool(os.environ.get("TAG_NO_FUSE")), "step_us": round(t * 1e3, 2)}),
+    print(json.dumps({"n": world, "gather": plans[0].info()["gather"], "recon_us": round(t * 1e3, 2)}),
           flush=True)
 g.close()
 for p in plans:
