@@ -152,8 +152,8 @@ typedef struct {
     int recon_bn;               /* output tile columns: 128 or 256                               */
     int recon_ctas;             /* 1: one CTA per 128-row tile; 2: CTA pair (tcgen05 cta_group::2,*/
                                 /*    256-row tiles)                                             */
-    int recon_box3d;            /* 1: each operand stage is one 3-D TMA box (CTA pairs, M and N  */
-                                /*    multiples of 64); 0: one 2-D box per 64-column chunk       */
+    int recon_box3d;            /* 1: each operand stage is one 3-D TMA box (bf16 factors, M and */
+                                /*    N multiples of 64); 0: one 2-D box per 64-column chunk     */
 } tag_plan_info_t;
 tag_status_t tag_sfb_plan_info(tag_sfb_plan_t plan, tag_plan_info_t* out);
 

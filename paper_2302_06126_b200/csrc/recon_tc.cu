@@ -8,7 +8,10 @@
 // X_all[k][m] with m contiguous, B_mma[j][k] = dY_all[k][j] with j contiguous — so no transpose
 // pass exists anywhere on the path. TMA loads 64-element (128-byte) MN chunks x BK rows with the
 // 128-byte swizzle; the UMMA descriptors describe the canonical MN-major SW128 layout
-// (LBO = stride between MN chunks, SBO = 1024 B between 8-row K groups).
+// (LBO = stride between MN chunks, SBO = 1024 B between 8-row K groups). When M and N are
+// multiples of 64, each operand's chunks of a stage arrive in ONE 3-D request instead of one per
+// chunk (a {64, K, M/64} view with a 128-byte chunk stride; fewer TMA instructions, measured
+// 1-2 us faster per bucket at K = 128, neutral elsewhere).
 //
 // Kernel structure (persistent, warp-specialised, one CTA per SM):
 //   warp 0      TMA producer: STAGES-deep smem ring of {A: 128 x BK, B: BN x BK} tiles
@@ -398,6 +401,12 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                             ptx::tma_load_2d_cg2(sb + c * C::CHUNK_BYTES, tmB, fbl, bn0 + C::ELEMS * c, kb * C::BK);
                     } else {
                         ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
+                        if (!X3 && gp.L[tr.li].box3) {
+                            ptx::tma_load_3d(sa, tmA, fb, 0, kb * C::BK, am0 / C::ELEMS);
+                            ptx::tma_load_3d(sb, tmB, fb, 0, kb * C::BK, bn0 / C::ELEMS);
+                            if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+                            continue;
+                        }
 #pragma unroll
                         for (int h = 0; h < C::HALVES; ++h) {     // X3: h = 1 loads the lo rows
                             const int kr = kb * C::BK + h * gp.L[tr.li].k_lo;
@@ -879,8 +888,7 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
             const char* e = std::getenv("TAG_RECON_NO3D");
             return e != nullptr && *e != 0;
         }();
-        L.box3 = CTAS == 2 && !X3 && !no3 && a[i].M % 64 == 0 && a[i].N % 64 == 0 &&
-                 a[i].lda % 64 == 0 ? 1 : 0;
+        L.box3 = !X3 && !no3 && a[i].M % 64 == 0 && a[i].N % 64 == 0 && a[i].lda % 64 == 0 ? 1 : 0;
         if (L.box3) {
             if (!encode_3d(&L.tmA, a[i].A, orows, a[i].M, C::BK, C::A_CHUNKS, a[i].lda) ||
                 !encode_3d(&L.tmB, a[i].Bm, orows, a[i].N, C::BK, C::B_CHUNKS))
@@ -1016,12 +1024,9 @@ void recon_tc_describe(const ReconArgs* a, int count, int* bn, int* ctas, int* b
     const bool wide = big_tiles(a, count);
     *bn = wide ? 256 : 128;
     *ctas = wide ? use_ctas(a, count) : 1;
-    *box3d = 0;
-    if (*ctas == 2) {
-        const char* e = std::getenv("TAG_RECON_NO3D");
-        const bool no3 = e != nullptr && *e != 0;
-        *box3d = !no3 && a[0].M % 64 == 0 && a[0].N % 64 == 0 && a[0].lda % 64 == 0 ? 1 : 0;
-    }
+    const char* e = std::getenv("TAG_RECON_NO3D");
+    const bool no3 = e != nullptr && *e != 0;
+    *box3d = !no3 && a[0].M % 64 == 0 && a[0].N % 64 == 0 && a[0].lda % 64 == 0 ? 1 : 0;
 }
 
 int recon_tc_grid(const ReconArgs* a, int count) {

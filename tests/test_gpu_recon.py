@@ -102,6 +102,16 @@ def test_pair_path_integer_bit_exact(tag, comm1, oracle_mod, shape, box3d, out_d
         f"max |diff| {np.abs(dW - want).max()}"
 
 
+@pytest.mark.parametrize("M,N,K,want", [(128, 256, 32, (128, 1, True)), (136, 264, 40, (128, 1, False)),
+                                         (4096, 4096, 128, (256, 1, True)),
+                                         (25088, 4096, 256, (256, 2, True))])
+def test_plan_info_tile_config(tag, comm1, M, N, K, want):
+    plan = tag.SfbPlan(comm1, M, N, K)
+    i = plan.info()
+    plan.close()
+    assert (i["recon_bn"], i["recon_ctas"], i["recon_box3d"]) == want, i
+
+
 @pytest.mark.parametrize("n,B", [(1, 32), (2, 32), (4, 32), (8, 32), (8, 64)])
 def test_virtual_n_random_vgg_fc7(tag, comm1, oracle_mod, n, B):
     """VGG-19 fc7 shape (4096 x 4096) at K = n*B: post-ReLU X, masked small dY (d-2 recipe)."""
