@@ -509,6 +509,31 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
             const float alpha = lp.alpha;
             const int n0 = tr.n0;
             const int row0 = tr.m0 + static_cast<int>(crank) * BM + 32 * quad;  // first row
+#ifndef EXP_OPT_PREFETCH
+#define EXP_OPT_PREFETCH 1
+#endif
+            if constexpr (SGD && EXP_OPT_PREFETCH) {
+                // The optimizer state this warp will update does not depend on the MMA: pull its
+                // rows (one per lane, GC columns) into L2 while the accumulator is still being
+                // computed, so the epilogue's W / v (/ m) loads hit L2 instead of HBM latency.
+                auto prefetch_tile = [&](int t) {
+                    const TileRef pr = locate<BN, CTAS>(gp, t);
+                    const LayerParams& pl = gp.L[pr.li];
+                    const int r = pr.m0 + static_cast<int>(crank) * BM + 32 * quad + static_cast<int>(lane);
+                    const int c0 = pr.n0 + half * GC;
+                    if (r < pl.M && c0 < pl.N) {
+                        const int64_t base = static_cast<int64_t>(r) * pl.N + c0;
+                        const int lines = ((pl.N - c0 < GC ? pl.N - c0 : GC) * 4 + 127) / 128;
+                        for (int j = 0; j < lines; ++j) {
+                            ptx::prefetch_l2(pl.W + base + 32 * j);
+                            ptx::prefetch_l2(pl.V + base + 32 * j);
+                            if (gp.opt == 2) ptx::prefetch_l2(pl.Mm + base + 32 * j);
+                        }
+                    }
+                };
+                if (EXP_OPT_PREFETCH == 1 || tile == unit) prefetch_tile(tile);
+                if (EXP_OPT_PREFETCH == 2 && tile + nunits < gp.num_tiles) prefetch_tile(tile + nunits);
+            }
             ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
             ptx::tc_fence_after();
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quad) << 16) + acc * C::ACC_COLS;
@@ -703,19 +728,26 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                             float4* wp4 = reinterpret_cast<float4*>(Wp + off0);
                             float4* vp4 = reinterpret_cast<float4*>(Vp + off0);
                             const int64_t gstep = step / 4;
-                            float4 wv[8], vv[8];
+#ifndef EXP_SGD_ROWS
+#define EXP_SGD_ROWS 4
+#endif
+                            constexpr int RW = EXP_SGD_ROWS;     // rows of W, v in flight
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                wv[i] = __ldcs(wp4 + i * gstep);
-                                vv[i] = __ldcs(vp4 + i * gstep);
+                            for (int h0 = 0; h0 < 8; h0 += RW) {
+                            float4 wv[RW], vv[RW];
+#pragma unroll
+                            for (int i = 0; i < RW; ++i) {
+                                wv[i] = __ldcs(wp4 + (h0 + i) * gstep);
+                                vv[i] = __ldcs(vp4 + (h0 + i) * gstep);
                             }
 #pragma unroll
-                            for (int i = 0; i < 8; ++i) {
+                            for (int ii = 0; ii < RW; ++ii) {
+                                const int i = h0 + ii;
                                 uint32_t dw[4];
                                 ptx::ld_shared_v4(sq + i * 512 + ((i & 1) ? sw1 : sw0), dw[0],
                                                   dw[1], dw[2], dw[3]);
-                                float* wf = reinterpret_cast<float*>(&wv[i]);
-                                float* vf = reinterpret_cast<float*>(&vv[i]);
+                                float* wf = reinterpret_cast<float*>(&wv[ii]);
+                                float* vf = reinterpret_cast<float*>(&vv[ii]);
 #pragma unroll
                                 for (int e = 0; e < 4; ++e) {
                                     // E2 (R14): g = dW + wd*W ; v = mu*v + g ; W -= lr*v
@@ -723,11 +755,12 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                                     vf[e] = __fadd_rn(__fmul_rn(mu, vf[e]), g);
                                     wf[e] = __fsub_rn(wf[e], __fmul_rn(lr, vf[e]));
                                 }
-                                __stcs(wp4 + i * gstep, wv[i]);
-                                __stcs(vp4 + i * gstep, vv[i]);
+                                __stcs(wp4 + i * gstep, wv[ii]);
+                                __stcs(vp4 + i * gstep, vv[ii]);
                                 if (Cp != nullptr)
                                     __stcs(reinterpret_cast<uint4*>(Cp + (off0 + i * step) * ESZ),
                                            make_uint4(dw[0], dw[1], dw[2], dw[3]));
+                            }
                             }
                             continue;
                         }
