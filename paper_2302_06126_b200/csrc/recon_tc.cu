@@ -55,6 +55,9 @@ constexpr int SMEM_MAX = 232448;              // 227 KB of dynamic shared memory
 constexpr int TMEM_COLS = 512;
 // Diagnostics only (scripts/build_variant.sh, never the product build): 1 = epilogue skips the
 // global stores, 2 = epilogue releases each accumulator without reading it
+#ifndef EXP_SGD_EP
+#define EXP_SGD_EP 1      // epilogue chunks per round in the optimizer instantiations
+#endif
 #ifndef EXP_EPI_MODE
 #define EXP_EPI_MODE 0
 #endif
@@ -291,7 +294,7 @@ template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const int me)
 {
-    constexpr int EP = OUT_BF16 || SGD || X3 ? 1 : 2;   // epilogue chunks per round
+    constexpr int EP = OUT_BF16 || X3 ? 1 : (SGD ? EXP_SGD_EP : 2);   // epilogue chunks per round
     using C = Cfg<BN, CTAS, X3, EP>;
     static_assert(!X3 || (CTAS == 1 && !FUSED), "3xTF32: single-CTA tiles, staged gather");
     static_assert(C::SMEM <= SMEM_MAX, "shared memory budget");
@@ -882,13 +885,17 @@ bool use_wide(const ReconArgs* a, int count) {
     // K = 192): the operand re-reads from L2 bind first there (fc6 at K = 256, one CTA: 102 us
     // at BN = 128, 88 us at BN = 256 with L2 throughput saturated); the pair halves B's again.
     bool wide = kmax >= 96;
-    if (const char* e = std::getenv("TAG_RECON_BN")) wide = std::atoi(e) == 256;   // experiments
+    // Optimizer epilogues (16-24 B of HBM traffic per dW element) stay on 128 x 128 tiles up to
+    // K = 512: BERT-L E2 bucket (scripts/sgd_bucket_time.py) 31.7 / 33.8 / 35.9 us at K = 128 /
+    // 256 / 512 vs 35.7 / 37.9 / 40.0 with wide tiles; at K = 1024 wide pairs win (42.0 vs 46.0)
+    if (a[0].sgd) wide = kmax > 512;
+    if (const char* e = std::getenv("TAG_RECON_BN"); e && *e) wide = std::atoi(e) == 256;   // experiments
     return wide;
 }
 
 int use_ctas(const ReconArgs* a, int count) {
     if (!use_wide(a, count)) return 1;
-    if (const char* e = std::getenv("TAG_RECON_CTAS")) return std::atoi(e) == 1 ? 1 : 2;
+    if (const char* e = std::getenv("TAG_RECON_CTAS"); e && *e) return std::atoi(e) == 1 ? 1 : 2;
     int64_t kmax = 0;
     for (int i = 0; i < count; ++i) kmax = a[i].K > kmax ? a[i].K : kmax;
     // measured on the VGG-19 bucket (scripts/tile_sweep.py): K = 128 one CTA x 256 columns 96 us
@@ -900,14 +907,14 @@ int use_ctas(const ReconArgs* a, int count) {
 // (e.g. Transformer FFN at K = 256: 16 pair tiles) runs faster on 4x as many 128 x 128 tiles.
 bool big_tiles(const ReconArgs* a, int count) {
     if (!use_wide(a, count)) return false;
-    if (std::getenv("TAG_RECON_BN")) return true;     // experiments force the wide config
+    if (const char* e = std::getenv("TAG_RECON_BN"); e && *e) return true;   // experiments force it
     const int ctas = use_ctas(a, count);
     return tiles_for(a, count, 256, ctas) >= num_sms() / ctas;
 }
 
 template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3 = false>
 tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
-    using C = Cfg<BN, CTAS, X3, (OUT_BF16 || SGD || X3 ? 1 : 2)>;
+    using C = Cfg<BN, CTAS, X3, (OUT_BF16 || X3 ? 1 : (SGD ? EXP_SGD_EP : 2))>;
     GroupParams gp;
     std::memset(&gp, 0, sizeof gp);
     int tiles = 0;
