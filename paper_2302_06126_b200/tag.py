@@ -225,6 +225,13 @@ class SfbPlan:
         _check(_lib.tag_sfb_plan(comm.handle, ctypes.byref(d), ctypes.byref(h)), "tag_sfb_plan")
         self._h = h
 
+    def _dev(self, t, dtype, shape, name):
+        ptr = _dev(t, dtype, shape, name)
+        if t.device.index != self.comm.device:
+            raise ValueError(f"{name} is on {t.device}, the plan's communicator uses "
+                             f"cuda:{self.comm.device}")
+        return ptr
+
     def info(self):
         i = PlanInfo()
         _check(_lib.tag_sfb_plan_info(self._h, ctypes.byref(i)), "tag_sfb_plan_info")
@@ -243,12 +250,12 @@ class SfbPlan:
         return _TORCH_DT[self.out_dtype]
 
     def _xy(self, X, dY):
-        return (_dev(X, self.in_torch, (self.B, self.M), "X"),
-                _dev(dY, self.in_torch, (self.B, self.N), "dY"))
+        return (self._dev(X, self.in_torch, (self.B, self.M), "X"),
+                self._dev(dY, self.in_torch, (self.B, self.N), "dY"))
 
     def sync(self, X, dY, dW, stream=None):
         x, dy = self._xy(X, dY)
-        _check(_lib.tag_sfb_sync(self._h, x, dy, _dev(dW, self.out_torch, (self.M, self.N), "dW"),
+        _check(_lib.tag_sfb_sync(self._h, x, dy, self._dev(dW, self.out_torch, (self.M, self.N), "dW"),
                                  _stream(stream)), "tag_sfb_sync")
         return dW
 
@@ -257,39 +264,39 @@ class SfbPlan:
         _check(_lib.tag_sfb_gather(self._h, x, dy, _stream(stream)), "tag_sfb_gather")
 
     def reconstruct(self, dW, stream=None):
-        _check(_lib.tag_sfb_reconstruct(self._h, _dev(dW, self.out_torch, (self.M, self.N), "dW"),
+        _check(_lib.tag_sfb_reconstruct(self._h, self._dev(dW, self.out_torch, (self.M, self.N), "dW"),
                                         _stream(stream)), "tag_sfb_reconstruct")
         return dW
 
     def bias_grad(self, db, stream=None):
         """db <- alpha * column sums of the dY_all of this plan's latest synchronisation."""
-        _check(_lib.tag_sfb_bias_grad(self._h, _dev(db, self.out_torch, (self.N,), "db"),
+        _check(_lib.tag_sfb_bias_grad(self._h, self._dev(db, self.out_torch, (self.N,), "db"),
                                       _stream(stream)), "tag_sfb_bias_grad")
         return db
 
     def sync_sgd(self, X, dY, W, v, dW=None, stream=None):
         x, dy = self._xy(X, dY)
         shape = (self.M, self.N)
-        dw = _dev(dW, self.out_torch, shape, "dW") if dW is not None else _vp()
-        _check(_lib.tag_sfb_sync_sgd(self._h, x, dy, _dev(W, torch.float32, shape, "W"),
-                                     _dev(v, torch.float32, shape, "v"), dw, _stream(stream)),
+        dw = self._dev(dW, self.out_torch, shape, "dW") if dW is not None else _vp()
+        _check(_lib.tag_sfb_sync_sgd(self._h, x, dy, self._dev(W, torch.float32, shape, "W"),
+                                     self._dev(v, torch.float32, shape, "v"), dw, _stream(stream)),
                "tag_sfb_sync_sgd")
 
     def sync_adam(self, X, dY, W, m, v, step, dW=None, stream=None):
         """tag_sfb_sync with Adam fused into the epilogue (step >= 1)."""
         x, dy = self._xy(X, dY)
         shape = (self.M, self.N)
-        dw = _dev(dW, self.out_torch, shape, "dW") if dW is not None else _vp()
-        _check(_lib.tag_sfb_sync_adam(self._h, x, dy, _dev(W, torch.float32, shape, "W"),
-                                      _dev(m, torch.float32, shape, "m"),
-                                      _dev(v, torch.float32, shape, "v"), step, dw,
+        dw = self._dev(dW, self.out_torch, shape, "dW") if dW is not None else _vp()
+        _check(_lib.tag_sfb_sync_adam(self._h, x, dy, self._dev(W, torch.float32, shape, "W"),
+                                      self._dev(m, torch.float32, shape, "m"),
+                                      self._dev(v, torch.float32, shape, "v"), step, dw,
                                       _stream(stream)), "tag_sfb_sync_adam")
 
     def adam_step(self, dW, W, m, v, step, stream=None):
         shape = (self.M, self.N)
-        _check(_lib.tag_adam_step(self._h, _dev(dW, torch.float32, shape, "dW"),
-                                  _dev(W, torch.float32, shape, "W"), _dev(m, torch.float32, shape, "m"),
-                                  _dev(v, torch.float32, shape, "v"), step, _stream(stream)),
+        _check(_lib.tag_adam_step(self._h, self._dev(dW, torch.float32, shape, "dW"),
+                                  self._dev(W, torch.float32, shape, "W"), self._dev(m, torch.float32, shape, "m"),
+                                  self._dev(v, torch.float32, shape, "v"), step, _stream(stream)),
                "tag_adam_step")
 
     def shard_rows(self, rank=None):
@@ -302,7 +309,7 @@ class SfbPlan:
     def sync_sharded(self, X, dY, dW_shard, stream=None):
         x, dy = self._xy(X, dY)
         _, rc = self.shard_rows()
-        dw = _dev(dW_shard, self.out_torch, (rc, self.N), "dW_shard") if rc > 0 else _vp()
+        dw = self._dev(dW_shard, self.out_torch, (rc, self.N), "dW_shard") if rc > 0 else _vp()
         _check(_lib.tag_sfb_sync_sharded(self._h, x, dy, dw, _stream(stream)),
                "tag_sfb_sync_sharded")
         return dW_shard
@@ -317,26 +324,26 @@ class SfbPlan:
 
     def local_grad(self, X, dY, dW, stream=None):
         x, dy = self._xy(X, dY)
-        _check(_lib.tag_local_grad(self._h, x, dy, _dev(dW, self.out_torch, (self.M, self.N), "dW"),
+        _check(_lib.tag_local_grad(self._h, x, dy, self._dev(dW, self.out_torch, (self.M, self.N), "dW"),
                                    _stream(stream)), "tag_local_grad")
         return dW
 
     def dense_allreduce(self, dW, stream=None):
-        _check(_lib.tag_dense_allreduce(self._h, _dev(dW, self.out_torch, (self.M, self.N), "dW"),
+        _check(_lib.tag_dense_allreduce(self._h, self._dev(dW, self.out_torch, (self.M, self.N), "dW"),
                                         _stream(stream)), "tag_dense_allreduce")
         return dW
 
     def ps_sync(self, dW, root, stream=None):
         """Replicate-with-PS: reduce to `root` (PreMulSum 1/(nB)) and broadcast back, in place."""
-        _check(_lib.tag_ps_sync(self._h, _dev(dW, self.out_torch, (self.M, self.N), "dW"), root,
+        _check(_lib.tag_ps_sync(self._h, self._dev(dW, self.out_torch, (self.M, self.N), "dW"), root,
                                 _stream(stream)), "tag_ps_sync")
         return dW
 
     def sgd_step(self, dW, W, v, stream=None):
         shape = (self.M, self.N)
-        _check(_lib.tag_sgd_step(self._h, _dev(dW, torch.float32, shape, "dW"),
-                                 _dev(W, torch.float32, shape, "W"),
-                                 _dev(v, torch.float32, shape, "v"), _stream(stream)),
+        _check(_lib.tag_sgd_step(self._h, self._dev(dW, torch.float32, shape, "dW"),
+                                 self._dev(W, torch.float32, shape, "W"),
+                                 self._dev(v, torch.float32, shape, "v"), _stream(stream)),
                "tag_sgd_step")
 
     def close(self):
@@ -360,11 +367,11 @@ class SfbGroup:
         out = []
         for p, t in zip(self.plans, ts):
             if which == "X":
-                out.append(_dev(t, p.in_torch, (p.B, p.M), "X"))
+                out.append(self.plans[0]._dev(t, p.in_torch, (p.B, p.M), "X"))
             elif which == "dY":
-                out.append(_dev(t, p.in_torch, (p.B, p.N), "dY"))
+                out.append(self.plans[0]._dev(t, p.in_torch, (p.B, p.N), "dY"))
             else:
-                out.append(_dev(t, p.out_torch, (p.M, p.N), "dW"))
+                out.append(self.plans[0]._dev(t, p.out_torch, (p.M, p.N), "dW"))
         assert len(out) == len(self.plans), f"{which}: one tensor per plan"
         return (_vp * len(out))(*out)
 
@@ -376,22 +383,22 @@ class SfbGroup:
         ptrs = []
         for p, t in zip(self.plans, dW_shards):
             _, rc = p.shard_rows()
-            ptrs.append(_dev(t, p.out_torch, (rc, p.N), "dW_shard") if rc > 0 else _vp())
+            ptrs.append(self.plans[0]._dev(t, p.out_torch, (rc, p.N), "dW_shard") if rc > 0 else _vp())
         _check(_lib.tag_sfb_group_sync_sharded(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"),
                                                (_vp * len(ptrs))(*ptrs), _stream(stream)),
                "tag_sfb_group_sync_sharded")
 
     def sync_sgd(self, Xs, dYs, Ws, vs, dWs=None, stream=None):
         shapes = [(p.M, p.N) for p in self.plans]
-        W = (_vp * len(self.plans))(*[_dev(w, torch.float32, s, "W") for w, s in zip(Ws, shapes)])
-        v = (_vp * len(self.plans))(*[_dev(x, torch.float32, s, "v") for x, s in zip(vs, shapes)])
+        W = (_vp * len(self.plans))(*[self.plans[0]._dev(w, torch.float32, s, "W") for w, s in zip(Ws, shapes)])
+        v = (_vp * len(self.plans))(*[self.plans[0]._dev(x, torch.float32, s, "v") for x, s in zip(vs, shapes)])
         dW = self._ptrs(dWs, "dW") if dWs is not None else None
         _check(_lib.tag_sfb_group_sync_sgd(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"), W,
                                            v, dW, _stream(stream)), "tag_sfb_group_sync_sgd")
 
     def sync_adam(self, Xs, dYs, Ws, ms, vs, step, dWs=None, stream=None):
         shapes = [(p.M, p.N) for p in self.plans]
-        arr = lambda ts, nm: (_vp * len(self.plans))(*[_dev(t, torch.float32, s_, nm)   # noqa: E731
+        arr = lambda ts, nm: (_vp * len(self.plans))(*[self.plans[0]._dev(t, torch.float32, s_, nm)   # noqa: E731
                                                       for t, s_ in zip(ts, shapes)])
         dW = self._ptrs(dWs, "dW") if dWs is not None else None
         _check(_lib.tag_sfb_group_sync_adam(self._h, self._ptrs(Xs, "X"), self._ptrs(dYs, "dY"),
@@ -407,7 +414,7 @@ class SfbGroup:
                "tag_sfb_group_reconstruct")
 
     def bias_grad(self, dbs, stream=None):
-        ptrs = [_dev(t, p.out_torch, (p.N,), "db") for p, t in zip(self.plans, dbs)]
+        ptrs = [self.plans[0]._dev(t, p.out_torch, (p.N,), "db") for p, t in zip(self.plans, dbs)]
         assert len(ptrs) == len(self.plans), "db: one tensor per plan"
         _check(_lib.tag_sfb_group_bias_grad(self._h, (_vp * len(ptrs))(*ptrs), _stream(stream)),
                "tag_sfb_group_bias_grad")
