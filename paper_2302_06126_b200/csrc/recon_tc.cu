@@ -73,7 +73,7 @@ constexpr int TMEM_COLS = 512;
 // HBM write binds. Stages carry 16 fp32 rows (32-element MN chunks of 128 B) of all four operands.
 // EP = epilogue chunks staged per round (2 for the fp32 E1 store, 1 for bf16 / E2 / X3), which
 // sizes the per-warp transpose buffers; the operand ring takes the rest of shared memory.
-template <int BN, int CTAS, bool X3 = false, int EP = 2>
+template <int BN, int CTAS, bool X3 = false, int EP = 2, bool LONGK = false>
 struct Cfg {
     // X3 keeps two accumulators per tile: hi*hi, and the small hi*lo + lo*hi terms apart, so the
     // big accumulator sees K/8 additions instead of 3K/8 (the tensor core's fp32 accumulation
@@ -81,10 +81,14 @@ struct Cfg {
     static constexpr int ACC_COLS = X3 ? 2 * BN : BN;     // TMEM columns per tile
     static constexpr int ACC = TMEM_COLS / ACC_COLS;      // accumulator buffers in TMEM
     static constexpr int ELEMS = X3 ? 32 : 64;            // MN elements per 128-byte chunk
-    // factor rows per pipeline stage. CTA pairs (K >= 192) load 64-row boxes: 8 KB per TMA
-    // request instead of 4 KB (fc6 at K = 256, bf16 dW: 68.3 -> 58.2 us; the per-request cost,
-    // not bytes, paced the operand stream)
-    static constexpr int BK = X3 ? 16 : (CTAS == 2 ? 64 : 32);
+    // factor rows per pipeline stage. CTA pairs (K >= 192) with a one-chunk epilogue (bf16 dW,
+    // optimizers) take 128 rows per stage (3 stages of 64 KB; with 3-D boxes one 32 KB TMA
+    // request per operand): fc6 at K = 256, bf16 dW, 32 / 64 / 128 rows: 74.6 / 60.1 / 58.1 us
+    // (the per-request cost, not bytes, paces the operand stream). With the two-chunk fp32
+    // epilogue only 2 such stages fit, which loses at large K (Transformer out-proj K = 2048:
+    // 78.8 vs 64.3 us), so those keep 64 rows (5 stages); so do K > 512 layers (LONGK: out-proj
+    // K = 2048, bf16 dW: 58.3 us with 64 rows, 60.4 with 128).
+    static constexpr int BK = X3 ? 16 : (CTAS == 2 ? (EP == 1 && !LONGK ? 128 : 64) : 32);
     static constexpr int KMMA = X3 ? 8 : 16;              // K per tcgen05.mma
     static constexpr int CHUNK_BYTES = BK * 128;          // one 128-byte-wide MN chunk of BK rows
     static constexpr int A_CHUNKS = BM / ELEMS;
@@ -99,8 +103,8 @@ struct Cfg {
     static constexpr int EPI_BUF_BYTES = EP * EPI_CHUNK_BYTES;   // per epilogue warp
     static constexpr int EPI_BYTES = NUM_EPI_WARPS * EPI_BUF_BYTES;
     static constexpr int BAR_BYTES = 256;
-    // as many stages as fit, at most 8 (BN = 128: 8; BN = 256 one CTA: 6; pairs: 5, or 6 with a
-    // one-chunk epilogue)
+    // as many stages as fit, at most 8 (BN = 128: 8; BN = 256 one CTA: 6; pairs: 3 with a
+    // one-chunk epilogue, 2 with the two-chunk fp32 one)
     static constexpr int FIT = (SMEM_MAX - 1024 - EPI_BYTES - BAR_BYTES) / STAGE_BYTES;
     static constexpr int STAGES = X3 ? 4 : (FIT < 8 ? FIT : 8);
     static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES;
@@ -290,12 +294,12 @@ __device__ __forceinline__ void fused_wait(const LayerParams& L, int me) {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3>
+template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3, bool LONGK>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const int me)
 {
     constexpr int EP = OUT_BF16 || X3 ? 1 : (SGD ? EXP_SGD_EP : 2);   // epilogue chunks per round
-    using C = Cfg<BN, CTAS, X3, EP>;
+    using C = Cfg<BN, CTAS, X3, EP, LONGK>;
     static_assert(!X3 || (CTAS == 1 && !FUSED), "3xTF32: single-CTA tiles, staged gather");
     static_assert(C::SMEM <= SMEM_MAX, "shared memory budget");
     extern __shared__ uint8_t smem_raw[];
@@ -912,9 +916,10 @@ bool big_tiles(const ReconArgs* a, int count) {
     return tiles_for(a, count, 256, ctas) >= num_sms() / ctas;
 }
 
-template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3 = false>
+template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3 = false,
+          bool LONGK = false>
 tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
-    using C = Cfg<BN, CTAS, X3, (OUT_BF16 || X3 ? 1 : (SGD ? EXP_SGD_EP : 2))>;
+    using C = Cfg<BN, CTAS, X3, (OUT_BF16 || X3 ? 1 : (SGD ? EXP_SGD_EP : 2)), LONGK>;
     GroupParams gp;
     std::memset(&gp, 0, sizeof gp);
     int tiles = 0;
@@ -984,7 +989,7 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     gp.cast = FUSED && fg->cast ? 1 : 0;
     gp.local_ctr = FUSED ? fg->local_ctr : nullptr;
     gp.local_target = FUSED ? fg->local_target : 0;
-    auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED, X3>;
+    auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED, X3, LONGK>;
     static bool attr_set = false;   // per instantiation
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1024,13 +1029,18 @@ tag_status_t dispatch(const ReconArgs* a, int count, cudaStream_t s, const Fused
     }
     const bool wide = big_tiles(a, count);
     const bool pair = wide && use_ctas(a, count) == 2;
+    int64_t kmax = 0;
+    for (int i = 0; i < count; ++i) kmax = a[i].K > kmax ? a[i].K : kmax;
+    const bool longk = kmax > 512;        // CTA-pair stages of 64 instead of 128 rows (see Cfg)
     if (a[0].sgd) {
         if (!wide) return launch_t<128, 1, false, true, FUSED>(a, count, s, fg);
+        if (pair && longk) return launch_t<256, 2, false, true, FUSED, false, true>(a, count, s, fg);
         return pair ? launch_t<256, 2, false, true, FUSED>(a, count, s, fg)
                     : launch_t<256, 1, false, true, FUSED>(a, count, s, fg);
     }
     if (a[0].out == TAG_BF16) {
         if (!wide) return launch_t<128, 1, true, false, FUSED>(a, count, s, fg);
+        if (pair && longk) return launch_t<256, 2, true, false, FUSED, false, true>(a, count, s, fg);
         return pair ? launch_t<256, 2, true, false, FUSED>(a, count, s, fg)
                     : launch_t<256, 1, true, false, FUSED>(a, count, s, fg);
     }

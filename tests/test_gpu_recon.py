@@ -82,8 +82,8 @@ def test_integer_inputs_bit_exact(tag, comm1, oracle_mod, M, N, K, out_dt):
 
 
 # CTA-pair shapes (>= 74 pair tiles, K >= 192): 3-D boxes with ragged n-block and K tails, and
-# 2-D boxes (M not a multiple of 64) with ragged M, N and K
-PAIR_SHAPES = [((4352, 2112, 264), True), ((4104, 2008, 200), False)]
+# 2-D boxes (M not a multiple of 64) with ragged M, N and K; K > 512 takes 64-row stages
+PAIR_SHAPES = [((4352, 2112, 264), True), ((4104, 2008, 200), False), ((4352, 2112, 600), True)]
 
 
 @pytest.mark.parametrize("shape,box3d", PAIR_SHAPES)
