@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -990,12 +991,16 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     gp.local_ctr = FUSED ? fg->local_ctr : nullptr;
     gp.local_target = FUSED ? fg->local_target : 0;
     auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED, X3, LONGK>;
-    static bool attr_set = false;   // per instantiation
-    if (!attr_set) {
+    // the shared-memory opt-in, once per instantiation and device (thread-safe)
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & bit)) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recon_tc)");
-        attr_set = true;
+        attr_set.fetch_or(bit, std::memory_order_release);
     }
     const int units = num_sms() / CTAS;     // one CTA (pair) per SM (TPC)
     cudaLaunchConfig_t cfg{};
