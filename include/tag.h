@@ -148,7 +148,8 @@ typedef struct {
     float alpha;                /* fl32(1/(nB)), the fused epilogue scale                       */
     int multicast;              /* 1: the fused push uses NVLS multimem stores (one store reaches */
                                 /*    every GPU); 0: one unicast store per peer                   */
-    /* the tensor-core launch this plan's reconstruction uses alone (0 when tensor_cores == 0): */
+    /* the tensor-core launch this plan's reconstruction uses alone — its fused optimizer      */
+    /* epilogue's launch when fuse_sgd / fuse_adam is set (0 when tensor_cores == 0):          */
     int recon_bn;               /* output tile columns: 128 or 256                               */
     int recon_ctas;             /* 1: one CTA per 128-row tile; 2: CTA pair (tcgen05 cta_group::2,*/
                                 /*    256-row tiles)                                             */

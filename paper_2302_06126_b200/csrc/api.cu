@@ -672,6 +672,7 @@ tag_status_t tag_sfb_plan_info(tag_sfb_plan_t p, tag_plan_info_t* out) {
         a.K = p->K;
         a.wire = p->d.wire_dtype;
         a.out = p->d.out_dtype;
+        a.sgd = p->d.fuse_sgd || p->d.fuse_adam;   // the optimizer epilogue's tile rule
         recon_tc_describe(&a, 1, &out->recon_bn, &out->recon_ctas, &out->recon_box3d);
     }
     return TAG_OK;

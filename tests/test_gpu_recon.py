@@ -202,6 +202,31 @@ def test_local_grad_and_dense_n1(tag, comm1, oracle_mod):
     plan.close()
 
 
+@pytest.mark.parametrize("M,N,K,want", [(1024, 4096, 512, (128, 1)), (4096, 4096, 1024, (256, 2))])
+def test_fused_sgd_tile_configs_equal_unfused(tag, comm1, M, N, K, want):
+    """E2 on both optimizer tile rules (128 x 128 tiles up to K = 512, CTA pairs with 64-row
+    stages above): fused == reconstruct + tag_sgd_step, bit for bit, over two steps."""
+    rs = np.random.default_rng(79)
+    X = torch.from_numpy(rs.standard_normal((K, M)).astype(np.float32)).to(torch.bfloat16).cuda()
+    dY = torch.from_numpy(rs.standard_normal((K, N)).astype(np.float32)).to(torch.bfloat16).cuda()
+    W0 = torch.from_numpy((0.02 * rs.standard_normal((M, N))).astype(np.float32)).cuda()
+    hp = dict(lr=1e-3, momentum=0.9, weight_decay=1e-2)
+    p = tag.SfbPlan(comm1, M, N, K, fuse_sgd=True, **hp)
+    i = p.info()
+    assert (i["recon_bn"], i["recon_ctas"]) == want, i
+    W1, v1 = W0.clone(), torch.zeros_like(W0)
+    W2, v2 = W0.clone(), torch.zeros_like(W0)
+    dW = torch.empty_like(W0)
+    for _ in range(2):
+        p.sync_sgd(X, dY, W1, v1, None)
+        p.sync(X, dY, dW)
+        p.sgd_step(dW, W2, v2)
+    torch.cuda.synchronize()
+    p.close()
+    assert torch.equal(W1, W2) and torch.equal(v1, v2)
+    assert not torch.equal(W1, W0)
+
+
 def test_fused_sgd_matches_unfused_and_oracle(tag, comm1, oracle_mod):
     """E2: the fused epilogue equals reconstruct + tag_sgd_step bit for bit, and the fp64 oracle
     (BERT-L pooler shape, virtual n = 8, B = 2; lr 1e-3, mu 0.9, wd 1e-2)."""
@@ -522,9 +547,10 @@ ADAM_HP = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
 
 
 @pytest.mark.parametrize("M,N,K,wire", [(4096, 1000, 32, "bf16"), (1024, 4096, 128, "bf16"),
-                                         (4096, 4096, 256, "bf16"), (512, 1024, 32, "f32"),
+                                         (4096, 4096, 256, "bf16"), (4096, 4096, 1024, "bf16"),
+                                         (512, 1024, 32, "f32"),
                                          (130, 257, 10, "bf16"), (136, 264, 40, "bf16")])
-def test_adam_fused_equals_unfused(tag, comm1, M, N, K, wire):
+def test_adam_fused_equals_unfused(tag, comm1, M, N, K, wire):  # noqa: E302
     """E3 (tensor-core epilogue; SIMT shapes: reconstruction + unfused kernel) == tag_sfb_sync
     followed by tag_adam_step, bit for bit, over three steps (one CTA, CTA pairs, 3xTF32)."""
     rs = np.random.default_rng(73)
