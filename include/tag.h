@@ -97,9 +97,28 @@ uint64_t tag_kernel_launches(void);
 tag_status_t tag_get_unique_id(unsigned char id[128]);
 /* COLLECTIVE. Sets the CUDA device to `cuda_device` for the calling thread and creates the NCCL
  * communicator of `nranks` ranks. nranks == 1 is valid and creates no NCCL communicator (`id` may
- * be NULL then). *out is set only on success. */
+ * be NULL then): plans on it skip the exchange entirely. *out is set only on success.
+ * Equivalent to tag_comm_create_ex(..., TAG_COMM_DEFAULT, out). */
 tag_status_t tag_comm_create(const unsigned char id[128], int nranks, int rank, int cuda_device,
                              tag_comm_t* out);
+typedef enum {
+    TAG_COMM_DEFAULT = 0,
+    /* NVLink SHARP: the fused push stores once to the multicast address of the LSA team instead
+     * of once per peer (needs NVLS; ignored when unavailable). Same results, bit for bit. */
+    TAG_COMM_NVLS_MULTICAST = 1,
+    /* nranks == 1 only: create a real one-rank NCCL communicator (device communicator, symmetric
+     * windows, PreMulSum op) so that every collective code path of the library runs with n = 1:
+     * the fused push into the (own) window with its arrival counters, the push-gather kernel and
+     * its LSA barrier, ncclAllGather, the PreMulSum ncclAllReduce, the PS reduce + broadcast and
+     * the sharded calls. Results equal those of the plain one-rank comm (the same values, since
+     * the exchange of one rank is a copy). `id` may be NULL (the library makes one). */
+    TAG_COMM_LOOPBACK = 2
+} tag_comm_flags_t;
+/* COLLECTIVE. tag_comm_create with flags (a bitwise OR of tag_comm_flags_t; every rank must pass
+ * the same flags). Errors: TAG_ERR_INVALID_ARG (unknown flag, bad rank/device, NULL id with
+ * nranks > 1), TAG_ERR_NCCL. */
+tag_status_t tag_comm_create_ex(const unsigned char id[128], int nranks, int rank, int cuda_device,
+                                unsigned flags, tag_comm_t* out);
 /* COLLECTIVE. Destroys the communicator. NULL is a no-op. */
 tag_status_t tag_comm_destroy(tag_comm_t comm);
 tag_status_t tag_comm_info(tag_comm_t comm, int* nranks, int* rank, int* cuda_device);
@@ -126,18 +145,31 @@ typedef struct {
     int fuse_adam;           /* 1: tag_sfb_sync_adam applies Adam in the epilogue (R22);     */
                              /* exclusive with fuse_sgd; uses lr and weight_decay too        */
     float beta1, beta2, eps; /* Adam hyper-parameters (also read by tag_adam_step)           */
+    int gather;              /* tag_gather_request_t: how step a2 moves the factors (0 = auto)*/
 } tag_sfb_desc_t;
+
+/* tag_sfb_desc_t.gather (must be identical on every rank):
+ *   AUTO: NVLink push into the peers' symmetric windows when every rank is NVLink load/store
+ *         reachable and the factor rows are 16-byte multiples, else ncclAllGather;
+ *   NCCL: always ncclAllGather (pack first when casting) — the library-collective baseline;
+ *   PUSH: the NVLink push or TAG_ERR_UNSUPPORTED from tag_sfb_plan. */
+typedef enum {
+    TAG_GATHER_REQ_AUTO = 0,
+    TAG_GATHER_REQ_NCCL = 1,
+    TAG_GATHER_REQ_PUSH = 2
+} tag_gather_request_t;
 
 /* COLLECTIVE. Validates `desc`, allocates the gather buffers (n*B*M and n*B*N elements of the
  * wire dtype) and staging, and creates the PreMulSum(1/(nB)) NCCL op used by the dense path.
- * Errors: TAG_ERR_INVALID_ARG (bad dims/dtypes, n != comm size), TAG_ERR_OOM, TAG_ERR_NCCL. */
+ * Errors: TAG_ERR_INVALID_ARG (bad dims/dtypes, n != comm size, unknown gather request),
+ * TAG_ERR_UNSUPPORTED (gather = PUSH where the push is unavailable), TAG_ERR_OOM, TAG_ERR_NCCL. */
 tag_status_t tag_sfb_plan(tag_comm_t comm, const tag_sfb_desc_t* desc, tag_sfb_plan_t* out);
 /* COLLECTIVE. NULL is a no-op. The caller must ensure no work using the plan is still pending. */
 tag_status_t tag_sfb_plan_destroy(tag_sfb_plan_t plan);
 
 /* Which implementation a plan selected (host query, no device work). */
 typedef enum {
-    TAG_GATHER_NONE = 0,        /* n = 1: nothing to exchange                                  */
+    TAG_GATHER_NONE = 0,        /* one-rank comm without NCCL: nothing to exchange             */
     TAG_GATHER_NCCL = 1,        /* pack (if casting) + ncclAllGather                           */
     TAG_GATHER_NVLINK_PUSH = 2  /* fused pack+push into peers' symmetric windows + LSA barrier */
 } tag_gather_mode_t;
@@ -164,8 +196,8 @@ tag_status_t tag_sfb_plan_info(tag_sfb_plan_t plan, tag_plan_info_t* out);
  *   a2 gather : X_r and dY_r reach every replica over NVLink ("broadcast to all devices"):
  *               fused with a1 as a push into the peers' symmetric windows (NCCL device API,
  *               TAG_GATHER_NVLINK_PUSH), or an ncclAllGather (TAG_GATHER_NCCL) when the rows are
- *               not 16-byte multiples, the ranks are not all NVLink-reachable, or the environment
- *               sets TAG_GATHER=nccl;
+ *               not 16-byte multiples, the ranks are not all NVLink-reachable, or the descriptor
+ *               asks for it (desc.gather = TAG_GATHER_REQ_NCCL);
  *   a3 recon  : dW = alpha * X_all^T dY_all on the tensor cores (K = n*B), alpha = 1/(nB);
  *   a4 store  : dW_out <- dW in out_dtype (fused epilogue).
  * X: B x M, dY: B x N (in_dtype, device). dW_out: M x N (out_dtype, device), overwritten.

@@ -19,7 +19,7 @@
 
 namespace tag {
 // push_gather.cu
-tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, void** out);
+tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, bool multimem, void** out);
 void push_devcomm_destroy(ncclComm_t comm, void* dc);
 bool push_devcomm_all_lsa(const void* dc, int nranks);
 void* push_devcomm_mc_base(const void* dc);
@@ -80,7 +80,7 @@ __global__ void scale_bf16_kernel(__nv_bfloat16* p, int64_t len, float alpha) {
 using namespace tag;
 
 struct tag_comm_s {
-    ncclComm_t nccl = nullptr;   // nullptr when nranks == 1
+    ncclComm_t nccl = nullptr;   // nullptr for a plain one-rank comm (no collective at all)
     int nranks = 1, rank = 0, device = 0;
     void* devcomm = nullptr;     // ncclDevComm (device API: LSA pointers + barriers), or nullptr
     bool lsa_all = false;        // every rank is load/store reachable (one NVLink domain)
@@ -181,6 +181,9 @@ tag_status_t validate_desc(const tag_comm_s* c, const tag_sfb_desc_t* d) {
     if (d->fuse_sgd && !(std::isfinite(d->lr) && std::isfinite(d->momentum) &&
                          std::isfinite(d->weight_decay)))
         return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: non-finite SGD hyper-parameter");
+    if (d->gather != TAG_GATHER_REQ_AUTO && d->gather != TAG_GATHER_REQ_NCCL &&
+        d->gather != TAG_GATHER_REQ_PUSH)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_plan: unknown gather request");
     return TAG_OK;
 }
 
@@ -192,7 +195,12 @@ tag_status_t check_ptrs(const char* fn, std::initializer_list<const void*> ps) {
     return TAG_OK;
 }
 
-bool needs_gather_buffers(const tag_sfb_desc_t& d) { return d.n > 1 || d.in_dtype != d.wire_dtype; }
+// a plan on a communicator with NCCL (n > 1, or a one-rank loopback comm) exchanges its factors
+bool has_collective(const tag_comm_s* c) { return c->nccl != nullptr; }
+
+bool needs_gather_buffers(const tag_comm_s* c, const tag_sfb_desc_t& d) {
+    return has_collective(c) || d.in_dtype != d.wire_dtype;
+}
 
 // Every rank's device work up to here is complete and every rank has reached this point: the
 // window of a new plan is zeroed everywhere before any peer can push into it (a late memset
@@ -201,7 +209,7 @@ bool needs_gather_buffers(const tag_sfb_desc_t& d) { return d.n > 1 || d.in_dtyp
 tag_status_t quiesce_all_ranks(tag_comm_s* c, const char* where) {
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, where);
-    if (c->nranks > 1 && c->devcomm && c->lsa_all) {
+    if (c->devcomm && c->lsa_all) {
         TAG_TRY(launch_comm_barrier(c->devcomm, COMM_BARRIER_INDEX, nullptr));
         e = cudaDeviceSynchronize();
         if (e != cudaSuccess) return cuda_fail(e, where);
@@ -214,7 +222,7 @@ tag_status_t do_gather(tag_plan_s* p, const void* X, const void* dY, cudaStream_
     const tag_sfb_desc_t& d = p->d;
     const int64_t cx = d.B * d.M, cy = d.B * d.N;          // elements per replica
     const size_t ew = dtype_size(d.wire_dtype);
-    if (d.n == 1) {
+    if (!has_collective(p->comm)) {
         if (d.in_dtype == d.wire_dtype) {
             p->src_x = X;
             p->src_dy = dY;
@@ -352,13 +360,17 @@ tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int
 // Fused path (a1 + a2 + a3 + a4 in ONE kernel): every plan gathers by NVLink push without a cast
 // and reconstructs on the tensor cores. The reconstruction kernel pushes this rank's factors
 // into every peer's window and waits, per layer, on arrival counters before loading its tiles.
-bool fusable(const tag_plan_s* p, void* dW) {
+// The decision depends only on the plan's descriptor and the epilogue kind (every pointer has
+// been validated 16-byte aligned before), so it is the same on every rank: a rank taking the
+// fused kernel while a peer took the staged push would wait on a barrier nobody joins.
+// opt: 0 = E1 (scale + store), 1 = fused SGD-momentum, 2 = fused Adam.
+bool fusable(const tag_plan_s* p, void* dW, int opt = 0) {
     if (p->gather_mode != TAG_GATHER_NVLINK_PUSH || !p->use_tc) return false;
     if (p->d.wire_dtype != TAG_BF16) return false;           // 3xTF32 needs the split pass
     const bool same = p->d.in_dtype == p->d.wire_dtype;
     const bool cast = p->d.in_dtype == TAG_F32 && p->d.wire_dtype == TAG_BF16;
     if (!same && !cast) return false;
-    if (std::getenv("TAG_NO_FUSE")) return false;
+    if (EXP_NO_FUSE) return false;                           // diagnostics builds
     ReconArgs a{};
     a.A = p->win_base;
     a.Bm = p->win_base;
@@ -368,6 +380,15 @@ bool fusable(const tag_plan_s* p, void* dW) {
     a.K = p->K;
     a.wire = p->d.wire_dtype;
     a.out = p->d.out_dtype;
+    if (opt) {
+        // the optimizer epilogues store fp32 dW only; a bf16-dW plan takes the staged path
+        // whether or not this call passes dW_out (keeps the decision rank-independent)
+        if (p->d.out_dtype != TAG_F32) return false;
+        // W, v, m are caller pointers checked for alignment already; the window base stands in
+        a.sgd = true;
+        a.opt = opt;
+        a.W = a.V = a.Mm = static_cast<float*>(p->win_base);
+    }
     return recon_tc_ok(a);
 }
 
@@ -425,23 +446,19 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
             a[i].M = rc;
         }
     }
-    // hierarchical publish (default): the last CTA of every rank adds 1 per layer, so each
-    // counter grows by n per call; per-CTA publish (TAG_FUSED_HIER=0): by n * grid
-    static const bool hier = [] {
-        const char* e = std::getenv("TAG_FUSED_HIER");
-        return e ? std::atoi(e) != 0 : true;
-    }();
+    // hierarchical publish: the last CTA of every rank adds 1 per layer on every peer, so each
+    // arrival counter grows by exactly n per call whatever grid each rank launched (the local
+    // counter, which this rank's CTAs alone increment, tracks this rank's own grid)
     const uint32_t grid = static_cast<uint32_t>(recon_tc_grid(a, count));
-    const uint32_t inc = static_cast<uint32_t>(c->nranks) * (hier ? 1u : grid);
+    const uint32_t inc = static_cast<uint32_t>(c->nranks);
     for (int i = 0; i < count; ++i) a[i].flag_target = plans[i]->flag_total[plans[i]->parity] + inc;
     tag_plan_s* p0 = plans[0];
     FusedGather fg{c->nranks, c->rank, c->mc_base,
                    plans[0]->d.in_dtype == TAG_F32 && plans[0]->d.wire_dtype == TAG_BF16,
-                   hier ? reinterpret_cast<uint32_t*>(static_cast<char*>(p0->win_base) +
-                                                      p0->win_flag_off + 8 + 4 * p0->parity)
-                        : nullptr,
+                   reinterpret_cast<uint32_t*>(static_cast<char*>(p0->win_base) +
+                                               p0->win_flag_off + 8 + 4 * p0->parity),
                    p0->local_total[p0->parity] + grid};
-    if (hier) p0->local_total[p0->parity] += grid;
+    p0->local_total[p0->parity] += grid;
     TAG_TRY(launch_recon_tc_group(a, count, s, &fg));
     for (int i = 0; i < count; ++i) {
         tag_plan_s* p = plans[i];
@@ -489,10 +506,18 @@ tag_status_t tag_get_unique_id(unsigned char id[128]) {
 
 tag_status_t tag_comm_create(const unsigned char id[128], int nranks, int rank, int cuda_device,
                              tag_comm_t* out) {
+    return tag_comm_create_ex(id, nranks, rank, cuda_device, TAG_COMM_DEFAULT, out);
+}
+
+tag_status_t tag_comm_create_ex(const unsigned char id[128], int nranks, int rank, int cuda_device,
+                                unsigned flags, tag_comm_t* out) {
     if (!out) return fail(TAG_ERR_INVALID_ARG, "tag_comm_create: NULL out");
     if (nranks < 1 || rank < 0 || rank >= nranks || cuda_device < 0)
         return fail(TAG_ERR_INVALID_ARG, "tag_comm_create: bad nranks/rank/device");
+    if (flags & ~static_cast<unsigned>(TAG_COMM_NVLS_MULTICAST | TAG_COMM_LOOPBACK))
+        return fail(TAG_ERR_INVALID_ARG, "tag_comm_create_ex: unknown flag");
     if (nranks > 1 && !id) return fail(TAG_ERR_INVALID_ARG, "tag_comm_create: NULL id");
+    const bool loopback = nranks == 1 && (flags & TAG_COMM_LOOPBACK);
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
@@ -503,16 +528,19 @@ tag_status_t tag_comm_create(const unsigned char id[128], int nranks, int rank, 
     c->nranks = nranks;
     c->rank = rank;
     c->device = cuda_device;
-    if (nranks > 1) {
+    if (nranks > 1 || loopback) {
         ncclUniqueId u;
-        std::memcpy(&u, id, 128);
-        ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+        ncclResult_t r = ncclSuccess;
+        if (id) std::memcpy(&u, id, 128);
+        else r = ncclGetUniqueId(&u);                       // loopback without an id
+        if (r == ncclSuccess) r = ncclCommInitRank(&c->nccl, nranks, u, rank);
         if (r != ncclSuccess) {
             delete c;
             return nccl_fail(r, "ncclCommInitRank");
         }
         // device API for the NVLink push gather; without it plans use ncclAllGather
-        if (push_devcomm_create(c->nccl, PUSH_MAX_CTAS + 1, &c->devcomm) == TAG_OK) {
+        if (push_devcomm_create(c->nccl, PUSH_MAX_CTAS + 1, (flags & TAG_COMM_NVLS_MULTICAST) != 0,
+                                &c->devcomm) == TAG_OK) {
             c->lsa_all = push_devcomm_all_lsa(c->devcomm, nranks);
             c->mc_base = push_devcomm_mc_base(c->devcomm);
         } else {
@@ -538,7 +566,7 @@ tag_status_t tag_comm_destroy(tag_comm_t c) {
 
 tag_status_t tag_comm_barrier(tag_comm_t c, tag_stream_t stream) {
     if (!c) return fail(TAG_ERR_INVALID_ARG, "tag_comm_barrier: NULL comm");
-    if (c->nranks == 1) return TAG_OK;
+    if (!has_collective(c)) return TAG_OK;
     TAG_TRY(set_device(c));
     TAG_TRY(check_async(c));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -569,7 +597,7 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
     // 4.8e-6 relative at K = 2048, 1.9e-5 at 8192 — and the fp32 bar is 1e-5, DESIGN R10)
     p->use_tc = d->M % 8 == 0 && d->N % 8 == 0 &&
                 (d->wire_dtype == TAG_BF16 ||
-                 (!std::getenv("TAG_F32_SIMT") && static_cast<int64_t>(d->n) * d->B <= 4096));
+                 (!EXP_F32_SIMT && static_cast<int64_t>(d->n) * d->B <= 4096));
     auto cleanup = [p]() {
         cudaFree(p->split);
         cudaFree(p->gx);
@@ -581,13 +609,18 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
         delete p;
     };
     const size_t ew = dtype_size(d->wire_dtype);
-    if (d->n > 1) {
-        const char* env = std::getenv("TAG_GATHER");
-        const bool want_nccl = env && std::strcmp(env, "nccl") == 0;
+    if (has_collective(c)) {
         const bool rows16 = (d->B * d->M * static_cast<int64_t>(ew)) % 16 == 0 &&
                             (d->B * d->N * static_cast<int64_t>(ew)) % 16 == 0;
-        p->gather_mode = (!want_nccl && c->devcomm && c->lsa_all && rows16) ? TAG_GATHER_NVLINK_PUSH
-                                                                             : TAG_GATHER_NCCL;
+        const bool push_ok = c->devcomm && c->lsa_all && rows16;
+        if (d->gather == TAG_GATHER_REQ_PUSH && !push_ok) {
+            delete p;
+            return fail(TAG_ERR_UNSUPPORTED, "tag_sfb_plan: NVLink push gather requested but not "
+                                             "available (ranks not all NVLink load/store reachable, "
+                                             "or factor rows not 16-byte multiples)");
+        }
+        p->gather_mode = (d->gather != TAG_GATHER_REQ_NCCL && push_ok) ? TAG_GATHER_NVLINK_PUSH
+                                                                       : TAG_GATHER_NCCL;
     }
     if (p->gather_mode == TAG_GATHER_NVLINK_PUSH) {
         p->win_buf_bytes = static_cast<size_t>(p->K * (d->M + d->N)) * ew;
@@ -621,7 +654,7 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
                 return cuda_fail(e, "tag_sfb_plan: cudaMalloc(local scratch)");
             }
         }
-    } else if (needs_gather_buffers(*d)) {
+    } else if (needs_gather_buffers(c, *d)) {
         cudaError_t e = cudaMalloc(&p->gx, static_cast<size_t>(p->K * d->M) * ew);
         if (e == cudaSuccess) e = cudaMalloc(&p->gdy, static_cast<size_t>(p->K * d->N) * ew);
         if (e != cudaSuccess) {
@@ -735,7 +768,7 @@ tag_status_t tag_sfb_sync_sgd(tag_sfb_plan_t p, const void* X, const void* dY, f
     TAG_TRY(set_device(p->comm));
     TAG_TRY(check_async(p->comm));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    if (fusable(p, dW_out)) return fused_sync(&p, 1, &X, &dY, &dW_out, true, &W, &v, s);
+    if (fusable(p, dW_out, 1)) return fused_sync(&p, 1, &X, &dY, &dW_out, true, &W, &v, s);
     TAG_TRY(do_gather(p, X, dY, s));
     return do_recon(p, dW_out, true, W, v, p->K, p->alpha, s);
 }
@@ -751,7 +784,7 @@ tag_status_t tag_sfb_sync_adam(tag_sfb_plan_t p, const void* X, const void* dY, 
     TAG_TRY(check_async(p->comm));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const AdamCall ad = adam_call(p->d, step);
-    if (fusable(p, dW_out)) return fused_sync(&p, 1, &X, &dY, &dW_out, true, &W, &v, s, false, &m, &ad);
+    if (fusable(p, dW_out, 2)) return fused_sync(&p, 1, &X, &dY, &dW_out, true, &W, &v, s, false, &m, &ad);
     TAG_TRY(do_gather(p, X, dY, s));
     return do_recon(p, dW_out, true, W, v, p->K, p->alpha, s, m, &ad);
 }
@@ -795,8 +828,9 @@ tag_status_t tag_sfb_sync_sharded(tag_sfb_plan_t p, const void* X, const void* d
     TAG_TRY(set_device(p->comm));
     TAG_TRY(check_async(p->comm));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    // the fused kernel needs at least one tile on every rank (its CTAs push the factors)
-    if (rc > 0 && fusable(p, dW_shard))
+    // the same route on every rank: a rank with an empty shard still launches the fused kernel
+    // (one push-only CTA), since its peers wait for its factors
+    if (fusable(p, rc > 0 ? dW_shard : nullptr))
         return fused_sync(&p, 1, &X, &dY, &dW_shard, false, nullptr, nullptr, s, true);
     TAG_TRY(do_gather(p, X, dY, s));
     if (rc == 0) return TAG_OK;
@@ -1093,7 +1127,7 @@ tag_status_t tag_sfb_group_sync_sgd(tag_sfb_group_t g, const void* const* X, con
     for (int i = 0; i < count; ++i) {
         TAG_TRY(check_ptrs("tag_sfb_group_sync_sgd", {X[i], dY[i], W[i], v[i]}));
         if (dWs[i]) TAG_TRY(check_ptrs("tag_sfb_group_sync_sgd", {dWs[i]}));
-        fuse = fuse && fusable(g->plans[i], dWs[i]);
+        fuse = fuse && fusable(g->plans[i], dWs[i], 1);
     }
     TAG_TRY(set_device(g->plans[0]->comm));
     TAG_TRY(check_async(g->plans[0]->comm));
@@ -1119,7 +1153,7 @@ tag_status_t tag_sfb_group_sync_adam(tag_sfb_group_t g, const void* const* X, co
     for (int i = 0; i < count; ++i) {
         TAG_TRY(check_ptrs("tag_sfb_group_sync_adam", {X[i], dY[i], W[i], m[i], v[i]}));
         if (dWs[i]) TAG_TRY(check_ptrs("tag_sfb_group_sync_adam", {dWs[i]}));
-        fuse = fuse && fusable(g->plans[i], dWs[i]);
+        fuse = fuse && fusable(g->plans[i], dWs[i], 2);
     }
     TAG_TRY(set_device(g->plans[0]->comm));
     TAG_TRY(check_async(g->plans[0]->comm));
@@ -1145,7 +1179,7 @@ tag_status_t tag_sfb_group_sync_sharded(tag_sfb_group_t g, const void* const* X,
         shard_range(g->plans[i], g->plans[i]->comm->rank, &rb, &rc);
         TAG_TRY(check_ptrs("tag_sfb_group_sync_sharded", {X[i], dY[i]}));
         if (rc > 0) TAG_TRY(check_ptrs("tag_sfb_group_sync_sharded", {dW[i]}));
-        fuse = fuse && rc > 0 && fusable(g->plans[i], dW[i]);
+        fuse = fuse && fusable(g->plans[i], rc > 0 ? dW[i] : nullptr);   // rank-independent
     }
     TAG_TRY(set_device(g->plans[0]->comm));
     TAG_TRY(check_async(g->plans[0]->comm));

@@ -54,8 +54,12 @@ struct PushGroup {
     int slot;               // this rank's slot (world rank)
 };
 
-// DBG (profiling only, TAG_PUSH_DEBUG): 1 = skip the data stores, 2 = skip the barrier,
-// 3 = full kernel + printf of %globaltimer phase stamps from a few CTAs.
+// DBG (diagnostics builds only: scripts/build_variant.sh -DEXP_PUSH_DBG=k, never the product):
+// 1 = skip the data stores, 2 = skip the barrier, 3 = full kernel + printf of %globaltimer phase
+// stamps from a few CTAs.
+#ifndef EXP_PUSH_DBG
+#define EXP_PUSH_DBG 0
+#endif
 __device__ __forceinline__ uint64_t gtimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -129,16 +133,15 @@ tag_status_t launch_comm_barrier(const void* dc, int index, cudaStream_t s) {
     return TAG_OK;
 }
 
-tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, void** out) {
+tag_status_t push_devcomm_create(ncclComm_t comm, int max_ctas, bool multimem, void** out) {
     ncclDevCommRequirements reqs;
     std::memset(&reqs, 0, sizeof reqs);
     reqs.lsaBarrierCount = max_ctas;
-    // NVLink SHARP multicast (one multimem store reaches every GPU): opt-in with TAG_MULTIMEM=1.
-    // Measured at n = 2 and 4 on B200 it is not faster than one unicast store per peer (the
-    // push is latency-bound: 8-11 us unicast vs 13-14 us multicast per CTA slice at n = 2).
-    // Collective: every rank must pass the same requirements.
-    const char* mm = std::getenv("TAG_MULTIMEM");
-    reqs.lsaMultimem = mm && std::strcmp(mm, "1") == 0;
+    // NVLink SHARP multicast (one multimem store reaches every GPU): opt-in with the comm flag
+    // TAG_COMM_NVLS_MULTICAST. Measured at n = 2 and 4 on B200 it is not faster than one unicast
+    // store per peer (the push is latency-bound: 8-11 us unicast vs 13-14 us multicast per CTA
+    // slice at n = 2). Collective: every rank must pass the same requirements.
+    reqs.lsaMultimem = multimem;
     ncclDevComm* dc = new ncclDevComm;
     ncclResult_t r = ncclDevCommCreate(comm, &reqs, dc);
     if (r != ncclSuccess) {
@@ -197,20 +200,10 @@ tag_status_t launch_push_gather_group(const void* dc, const PushSegment* seg, in
     g.total = total;
     g.slot = slot;
     const int grid = push_grid(total, max_ctas);
-    static const int dbg = [] {
-        const char* e = std::getenv("TAG_PUSH_DEBUG");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (dbg == 1)
-        push_gather_kernel<false, 1><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
-    else if (dbg == 2)
-        push_gather_kernel<false, 2><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
-    else if (dbg == 3)
-        push_gather_kernel<false, 3><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
-    else if (in == wire)
-        push_gather_kernel<false><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
+    if (in == wire)
+        push_gather_kernel<false, EXP_PUSH_DBG><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
     else
-        push_gather_kernel<true><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
+        push_gather_kernel<true, EXP_PUSH_DBG><<<grid, PUSH_THREADS, 0, s>>>(comm, g);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "launch push_gather_kernel");
     count_launch();

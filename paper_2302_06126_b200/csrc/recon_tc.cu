@@ -62,6 +62,21 @@ constexpr int TMEM_COLS = 512;
 #ifndef EXP_EPI_MODE
 #define EXP_EPI_MODE 0
 #endif
+// Diagnostics builds only: fused-exchange phases (see the kernel), forced tile shapes
+// (EXP_RECON_BN = 128 | 256, EXP_RECON_CTAS = 1 | 2; 0 = the measured rule), 2-D instead of
+// 3-D TMA boxes (EXP_RECON_NO3D), SIMT FFMA instead of 3xTF32 for fp32 factors (EXP_F32_SIMT).
+#ifndef EXP_FUSED_DBG
+#define EXP_FUSED_DBG 0
+#endif
+#ifndef EXP_RECON_BN
+#define EXP_RECON_BN 0
+#endif
+#ifndef EXP_RECON_CTAS
+#define EXP_RECON_CTAS 0
+#endif
+#ifndef EXP_RECON_NO3D
+#define EXP_RECON_NO3D 0
+#endif
 
 // CTAS = 2: a CTA pair on one TPC runs tcgen05 cta_group::2 — UMMA M = 256 (128 rows of A in
 // each CTA's smem), N = BN (BN/2 columns of B in each CTA's smem), each CTA's TMEM holds its
@@ -153,9 +168,8 @@ struct GroupParams {
     AdamConsts adam;
     int slot;              // this rank (its slot in X_all / dY_all)
     char* mc_base;         // FUSED: NVLS multicast base of the windows, or nullptr (unicast)
-    int dbg;               // TAG_FUSED_DEBUG (profiling only): 1 no push/wait, 2 no wait, 3 stamps
     int cast;              // FUSED: the sources are fp32, cast to bf16 (RNE) on the way out
-    uint32_t* local_ctr;   // FUSED: hierarchical publish (FusedGather::local_ctr) or nullptr
+    uint32_t* local_ctr;   // FUSED: hierarchical publish counter (FusedGather::local_ctr)
     uint32_t local_target;
 };
 
@@ -251,13 +265,14 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
         }
     }
     // One system-scope release for the whole slice (a fence per layer costs a NVLink round trip
-    // each), then relaxed increments of every layer's arrival counter on every peer — by every
-    // CTA, or (hierarchical) only by the last CTA of this rank to arrive on a local counter,
-    // which cuts the remote atomics landing on each counter from n * grid to n.
+    // each), then a hierarchical publish: every CTA adds 1 to a local counter and only the last
+    // CTA of this rank to arrive adds 1 to every layer's arrival counter on every peer, so each
+    // counter sees n remote atomics per call (not n * grid) and its target does not depend on
+    // the grid size (ranks may launch different grids, e.g. sharded with uneven shards).
     __syncthreads();
     if (threadIdx.x == 0) {
         asm volatile("fence.acq_rel.sys;" ::: "memory");
-        if (gp.local_ctr != nullptr) {
+        {
             uint32_t old;
             asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
                          : "=r"(old) : "l"(gp.local_ctr) : "memory");
@@ -327,6 +342,7 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
     // ---- prologue (overlaps the previous kernel's tail under programmatic dependent launch)
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < gp.count; ++i) {
+            if (gp.L[i].M == 0) continue;             // empty shard: no tensor maps
             ptx::tma_prefetch_desc(&gp.L[i].tmA);
             ptx::tma_prefetch_desc(&gp.L[i].tmB);
         }
@@ -351,11 +367,13 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
     const uint32_t tmem_base = *tmem_slot_ptr;
     // no global memory is touched before the previous grid in the stream has completed
     grid_dep_wait();
+    // Diagnostics builds only (scripts/build_variant.sh -DEXP_FUSED_DBG=k, never the product):
+    // 1 = no push and no wait, 2 = push without the arrival wait, 3 = printf phase stamps.
     uint64_t t_start = 0, t_pushed = 0;
     if constexpr (FUSED) {
-        if (gp.dbg == 3) t_start = gtimer();
-        if (gp.dbg != 1) fused_push(gp, npeers, me);
-        if (gp.dbg == 3) t_pushed = gtimer();
+        if (EXP_FUSED_DBG == 3) t_start = gtimer();
+        if (EXP_FUSED_DBG != 1) fused_push(gp, npeers, me);
+        if (EXP_FUSED_DBG == 3) t_pushed = gtimer();
     }
 
     if (warp == 0) {
@@ -368,9 +386,9 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                 const TileRef tr = locate<BN, CTAS>(gp, tile);
                 if constexpr (FUSED) {
                     if (!(ready & (1u << tr.li))) {
-                        if (gp.dbg == 0 || gp.dbg == 3) fused_wait(gp.L[tr.li], me);
-#ifdef TAG_FUSED_STAMPS   // profiling builds only: a printf in the kernel costs 1-2 us per launch
-                        if (gp.dbg == 3 && ready == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
+                        if (EXP_FUSED_DBG == 0 || EXP_FUSED_DBG == 3) fused_wait(gp.L[tr.li], me);
+#if EXP_FUSED_DBG == 3   // profiling builds only: a printf in the kernel costs 1-2 us per launch
+                        if (ready == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
                             printf("fused rank %d cta %d push %llu ns, wait-after-push %llu ns\n", me,
                                    blockIdx.x, (unsigned long long)(t_pushed - t_start),
                                    (unsigned long long)(gtimer() - t_pushed));
@@ -875,6 +893,15 @@ bool encode_3d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int 
     return r == CUDA_SUCCESS;
 }
 
+// one CTA (pair) per SM (TPC), at most one per tile; a FUSED launch keeps at least one unit even
+// with no tiles (every rank must push its factors)
+int grid_for(int tiles, int ctas, bool fused) {
+    const int units = num_sms() / ctas;
+    int g = tiles < units ? tiles : units;
+    if (fused && g < 1) g = 1;
+    return ctas * g;
+}
+
 int tiles_for(const ReconArgs* a, int count, int bn, int ctas) {
     int64_t tiles = 0;
     for (int i = 0; i < count; ++i)
@@ -894,13 +921,13 @@ bool use_wide(const ReconArgs* a, int count) {
     // K = 512: BERT-L E2 bucket (scripts/sgd_bucket_time.py) 31.7 / 33.8 / 35.9 us at K = 128 /
     // 256 / 512 vs 35.7 / 37.9 / 40.0 with wide tiles; at K = 1024 wide pairs win (42.0 vs 46.0)
     if (a[0].sgd) wide = kmax > 512;
-    if (const char* e = std::getenv("TAG_RECON_BN"); e && *e) wide = std::atoi(e) == 256;   // experiments
+    if (EXP_RECON_BN) wide = EXP_RECON_BN == 256;   // diagnostics builds
     return wide;
 }
 
 int use_ctas(const ReconArgs* a, int count) {
     if (!use_wide(a, count)) return 1;
-    if (const char* e = std::getenv("TAG_RECON_CTAS"); e && *e) return std::atoi(e) == 1 ? 1 : 2;
+    if (EXP_RECON_CTAS) return EXP_RECON_CTAS == 1 ? 1 : 2;   // diagnostics builds
     int64_t kmax = 0;
     for (int i = 0; i < count; ++i) kmax = a[i].K > kmax ? a[i].K : kmax;
     // measured on the VGG-19 bucket (scripts/tile_sweep.py): K = 128 one CTA x 256 columns 96 us
@@ -912,7 +939,7 @@ int use_ctas(const ReconArgs* a, int count) {
 // (e.g. Transformer FFN at K = 256: 16 pair tiles) runs faster on 4x as many 128 x 128 tiles.
 bool big_tiles(const ReconArgs* a, int count) {
     if (!use_wide(a, count)) return false;
-    if (const char* e = std::getenv("TAG_RECON_BN"); e && *e) return true;   // experiments force it
+    if (EXP_RECON_BN) return true;   // diagnostics builds force it
     const int ctas = use_ctas(a, count);
     return tiles_for(a, count, 256, ctas) >= num_sms() / ctas;
 }
@@ -930,12 +957,11 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
         const int oes = X3 ? 4 : 2;
         const int64_t orows = X3 ? 2 * a[i].kpad : a[i].K;      // X3: [hi ; lo], Kp rows each
         const CUtensorMapSwizzle oswz = X3 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B;
-        static const bool no3 = [] {                                         // experiments
-            const char* e = std::getenv("TAG_RECON_NO3D");
-            return e != nullptr && *e != 0;
-        }();
-        L.box3 = !X3 && !no3 && a[i].M % 64 == 0 && a[i].N % 64 == 0 && a[i].lda % 64 == 0 ? 1 : 0;
-        if (L.box3) {
+        L.box3 = !X3 && !EXP_RECON_NO3D && a[i].M % 64 == 0 && a[i].N % 64 == 0 && a[i].lda % 64 == 0 ? 1 : 0;
+        if (a[i].M == 0) {
+            // an empty row shard (sharded sync, more ranks than 128-row tiles): no tiles and no
+            // tensor maps; in a FUSED launch the layer's factors are still pushed to the peers
+        } else if (L.box3) {
             if (!encode_3d(&L.tmA, a[i].A, orows, a[i].M, C::BK, C::A_CHUNKS, a[i].lda) ||
                 !encode_3d(&L.tmB, a[i].Bm, orows, a[i].N, C::BK, C::B_CHUNKS))
                 return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed for the factor operands");
@@ -982,11 +1008,6 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
                          a[0].wd};
     gp.slot = FUSED ? fg->me : 0;
     gp.mc_base = FUSED ? static_cast<char*>(fg->mc_base) : nullptr;
-    static const int dbg = [] {
-        const char* e = std::getenv("TAG_FUSED_DEBUG");
-        return e ? std::atoi(e) : 0;
-    }();
-    gp.dbg = dbg;
     gp.cast = FUSED && fg->cast ? 1 : 0;
     gp.local_ctr = FUSED ? fg->local_ctr : nullptr;
     gp.local_target = FUSED ? fg->local_target : 0;
@@ -1002,9 +1023,8 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(recon_tc)");
         attr_set.fetch_or(bit, std::memory_order_release);
     }
-    const int units = num_sms() / CTAS;     // one CTA (pair) per SM (TPC)
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(CTAS * (tiles < units ? tiles : units)));
+    cfg.gridDim = dim3(static_cast<unsigned>(grid_for(tiles, CTAS, FUSED)));
     cfg.blockDim = dim3(NUM_THREADS);
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = s;
@@ -1058,7 +1078,7 @@ tag_status_t dispatch(const ReconArgs* a, int count, cudaStream_t s, const Fused
 
 bool recon_tc_ok(const ReconArgs& a) {
     if (a.wire == TAG_F32 && a.kpad < a.K) return false;  // 3xTF32 needs the split [hi ; lo] operands
-    if (a.wire == TAG_F32 && (std::getenv("TAG_F32_SIMT") || a.lda)) return false;
+    if (a.wire == TAG_F32 && (EXP_F32_SIMT || a.lda)) return false;
     if (a.M % 8 || a.N % 8 || a.lda % 8) return false;   // 16-byte rows for TMA (bf16)
     if (a.M > INT32_MAX || a.N > INT32_MAX || a.K > INT32_MAX) return false;
     if (a.sgd && a.out == TAG_BF16 && a.C) return false;  // E2 writes fp32 dW only
@@ -1079,17 +1099,13 @@ void recon_tc_describe(const ReconArgs* a, int count, int* bn, int* ctas, int* b
     const bool wide = big_tiles(a, count);
     *bn = wide ? 256 : 128;
     *ctas = wide ? use_ctas(a, count) : 1;
-    const char* e = std::getenv("TAG_RECON_NO3D");
-    const bool no3 = e != nullptr && *e != 0;
-    *box3d = !no3 && a[0].M % 64 == 0 && a[0].N % 64 == 0 && a[0].lda % 64 == 0 ? 1 : 0;
+    *box3d = !EXP_RECON_NO3D && a[0].M % 64 == 0 && a[0].N % 64 == 0 && a[0].lda % 64 == 0 ? 1 : 0;
 }
 
 int recon_tc_grid(const ReconArgs* a, int count) {
     const bool wide = big_tiles(a, count);
     const int ctas = wide ? use_ctas(a, count) : 1;
-    const int tiles = tiles_for(a, count, wide ? 256 : 128, ctas);
-    const int units = num_sms() / ctas;
-    return ctas * (tiles < units ? tiles : units);
+    return grid_for(tiles_for(a, count, wide ? 256 : 128, ctas), ctas, true);
 }
 
 tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s,

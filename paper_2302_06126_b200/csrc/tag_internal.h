@@ -7,6 +7,16 @@
 
 #include "../../include/tag.h"
 
+// Diagnostics builds only (scripts/build_variant.sh -D...; the product build never sets these):
+// EXP_F32_SIMT = fp32 factors on the SIMT FFMA kernel instead of 3xTF32; EXP_NO_FUSE = staged
+// push kernel + reconstruction instead of the fused exchange kernel.
+#ifndef EXP_F32_SIMT
+#define EXP_F32_SIMT 0
+#endif
+#ifndef EXP_NO_FUSE
+#define EXP_NO_FUSE 0
+#endif
+
 namespace tag {
 
 // Thread-local error detail behind tag_last_error().
@@ -61,7 +71,7 @@ struct FusedGather {
     bool cast;             // sources are fp32, the wire is bf16 (RNE cast inside the push)
     // hierarchical publish: CTAs count themselves on a local counter; the last one of this rank
     // adds 1 to every layer's counter on every peer (n remote atomics per layer, not n * grid)
-    uint32_t* local_ctr;   // device address (this rank's window) or nullptr = per-CTA publish
+    uint32_t* local_ctr;   // device address (this rank's window)
     uint32_t local_target; // local counter value after this launch's CTAs have all arrived
 };
 

@@ -47,15 +47,17 @@ def broadcast_bytes(payload, nbytes=128, src=0):
     return bytes(t.cpu().tolist())
 
 
-def bootstrap_comm(tag, local_rank):
-    """Create the libtag communicator over all ranks of the default group (n = world size)."""
+def bootstrap_comm(tag, local_rank, loopback=False, multicast=False):
+    """Create the libtag communicator over all ranks of the default group (n = world size).
+    loopback: with one rank, still create a (one-rank) NCCL communicator so the collective code
+    paths run; multicast: NVLS multicast stores in the fused push."""
     world = dist.get_world_size() if dist.is_initialized() else 1
     rank = dist.get_rank() if dist.is_initialized() else 0
     if world == 1:
-        return tag.Comm(1, 0, local_rank)
+        return tag.Comm(1, 0, local_rank, loopback=loopback, multicast=multicast)
     uid = tag.unique_id() if rank == 0 else bytes(128)
     uid = broadcast_bytes(uid, 128, 0)
-    return tag.Comm(world, rank, local_rank, uid)
+    return tag.Comm(world, rank, local_rank, uid, multicast=multicast)
 
 
 def max_over_ranks(x):

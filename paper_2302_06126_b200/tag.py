@@ -36,7 +36,7 @@ class SfbDesc(ctypes.Structure):
                 ("out_dtype", ctypes.c_int), ("fuse_sgd", ctypes.c_int), ("lr", ctypes.c_float),
                 ("momentum", ctypes.c_float), ("weight_decay", ctypes.c_float),
                 ("fuse_adam", ctypes.c_int), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float),
-                ("eps", ctypes.c_float)]
+                ("eps", ctypes.c_float), ("gather", ctypes.c_int)]
 
 
 class PlanInfo(ctypes.Structure):
@@ -48,6 +48,8 @@ class PlanInfo(ctypes.Structure):
 
 GATHER_NONE, GATHER_NCCL, GATHER_NVLINK_PUSH = 0, 1, 2
 GATHER_NAMES = {0: "none", 1: "nccl_allgather", 2: "nvlink_push"}
+GATHER_REQ = {"auto": 0, "nccl": 1, "push": 2}          # tag_gather_request_t
+COMM_DEFAULT, COMM_NVLS_MULTICAST, COMM_LOOPBACK = 0, 1, 2  # tag_comm_flags_t
 
 
 class LayerDesc(ctypes.Structure):
@@ -86,6 +88,7 @@ _SIGS = {
     "tag_kernel_launches": ([], ctypes.c_uint64),
     "tag_get_unique_id": ([ctypes.c_char_p], _st),
     "tag_comm_create": ([ctypes.c_char_p, _i, _i, _i, _p(_vp)], _st),
+    "tag_comm_create_ex": ([ctypes.c_char_p, _i, _i, _i, ctypes.c_uint, _p(_vp)], _st),
     "tag_comm_destroy": ([_vp], _st),
     "tag_comm_info": ([_vp, _p(_i), _p(_i), _p(_i)], _st),
     "tag_comm_barrier": ([_vp, _vp], _st),
@@ -184,15 +187,24 @@ def unique_id():
 
 
 class Comm:
-    """One process per GPU. nranks == 1 needs no id (no NCCL communicator is created)."""
+    """One process per GPU. nranks == 1 needs no id (no NCCL communicator is created unless
+    loopback=True: a real one-rank NCCL communicator, so every collective code path runs at n = 1).
+    multicast=True asks for NVLS multicast stores in the fused push (TAG_COMM_NVLS_MULTICAST)."""
 
-    def __init__(self, nranks, rank, device, uid=None):
+    def __init__(self, nranks, rank, device, uid=None, multicast=False, loopback=False):
         h = _vp()
         idbuf = ctypes.create_string_buffer(uid, 128) if uid is not None else None
-        _check(_lib.tag_comm_create(idbuf, nranks, rank, device, ctypes.byref(h)),
-               "tag_comm_create")
+        flags = (COMM_NVLS_MULTICAST if multicast else 0) | (COMM_LOOPBACK if loopback else 0)
+        _check(_lib.tag_comm_create_ex(idbuf, nranks, rank, device, flags, ctypes.byref(h)),
+               "tag_comm_create_ex")
         self._h = h
         self.nranks, self.rank, self.device = nranks, rank, device
+        self.loopback = bool(loopback and nranks == 1)
+
+    @classmethod
+    def loopback_comm(cls, device=0):
+        """One-rank comm with a real NCCL communicator (TAG_COMM_LOOPBACK)."""
+        return cls(1, 0, device, loopback=True)
 
     @property
     def handle(self):
@@ -213,14 +225,14 @@ class SfbPlan:
 
     def __init__(self, comm, M, N, B, in_dtype="bf16", wire_dtype="bf16", out_dtype="f32",
                  fuse_sgd=False, lr=0.0, momentum=0.0, weight_decay=0.0, fuse_adam=False,
-                 beta1=0.9, beta2=0.999, eps=1e-8):
+                 beta1=0.9, beta2=0.999, eps=1e-8, gather="auto"):
         self.comm = comm
         self.M, self.N, self.B, self.n = M, N, B, comm.nranks
         self.in_dtype, self.wire_dtype, self.out_dtype = (_DT_OF[in_dtype], _DT_OF[wire_dtype],
                                                           _DT_OF[out_dtype])
         d = SfbDesc(M, N, B, comm.nranks, self.in_dtype, self.wire_dtype, self.out_dtype,
                     1 if fuse_sgd else 0, lr, momentum, weight_decay, 1 if fuse_adam else 0,
-                    beta1, beta2, eps)
+                    beta1, beta2, eps, GATHER_REQ[gather])
         h = _vp()
         _check(_lib.tag_sfb_plan(comm.handle, ctypes.byref(d), ctypes.byref(h)), "tag_sfb_plan")
         self._h = h

@@ -1,7 +1,10 @@
 #!/usr/bin/env python3
 """Multi-GPU parity of the SFB path through the C ABI (run under torchrun, one process per GPU).
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port P scripts/multi_gpu_check.py
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port P scripts/multi_gpu_check.py \
+        [--gather auto|nccl|push] [--multicast]
+    python scripts/multi_gpu_check.py --loopback      (one GPU: a one-rank NCCL communicator, so
+                                                       every collective code path runs at n = 1)
 
 Checks, for n = world size ("MatMul ops on each device can reconstruct identical
 gradients"):
@@ -42,9 +45,16 @@ def rel_fro(a, r):
 
 
 def main():
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gather", default="auto", choices=["auto", "nccl", "push"])
+    ap.add_argument("--multicast", action="store_true")
+    ap.add_argument("--loopback", action="store_true")
+    args = ap.parse_args()
     rank, local_rank, world = tdist.init_from_env()
     torch.cuda.set_device(local_rank)
-    comm = tdist.bootstrap_comm(tag, local_rank)
+    comm = tdist.bootstrap_comm(tag, local_rank, loopback=args.loopback, multicast=args.multicast)
+    gather = args.gather
     n = world
     results = {}
     modes = set()
@@ -57,7 +67,7 @@ def main():
 
     def run(cid, li, M, N, B, xd, dyd, in_dt, wire_dt, out_dt):
         X, dY = synth.factors(cid, li, rank, M, N, B, xd, dyd)
-        plan = tag.SfbPlan(comm, M, N, B, in_dt, wire_dt, out_dt)
+        plan = tag.SfbPlan(comm, M, N, B, in_dt, wire_dt, out_dt, gather=gather)
         modes.add(plan.info()["gather"] + ("+multicast" if plan.info()["multicast"] else ""))
         Xd = torch.from_numpy(X).to(TDT[in_dt]).cuda()
         dYd = torch.from_numpy(dY).to(TDT[in_dt]).cuda()
@@ -124,7 +134,8 @@ def main():
     M, N, B = 1024, 1024, 2
     X, dY = synth.factors(5, 3, rank, M, N, B, "tanh", "small")
     W0, v0 = synth.sgd_state(5, 3, M, N)
-    plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", fuse_sgd=True, lr=1e-3, momentum=0.9)
+    plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", fuse_sgd=True, lr=1e-3, momentum=0.9,
+                       gather=gather)
     Xd, dYd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(dY).to(torch.bfloat16).cuda()
     W1, v1 = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
     for _ in range(3):
@@ -144,7 +155,7 @@ def main():
     X, dY = synth.factors(5, 4, rank, M, N, B, "normal", "small")
     W0, _ = synth.sgd_state(5, 4, M, N)
     plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", fuse_adam=True, lr=1e-3,
-                       weight_decay=0.01)
+                       weight_decay=0.01, gather=gather)
     Xd, dYd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(dY).to(torch.bfloat16).cuda()
     W1, m1, v1 = torch.from_numpy(W0).cuda(), torch.zeros(M, N, device="cuda"), torch.zeros(M, N, device="cuda")
     W2, m2, v2 = W1.clone(), m1.clone(), v1.clone()
@@ -159,13 +170,38 @@ def main():
            and len(set(hashes)) == 1)
     plan.close()
 
+    # 6c: fused SGD with a bf16 dW_out (the optimizer epilogue stores fp32 dW only, so this plan
+    #     takes the staged path on every rank): integer inputs make dW exact, so W, v equal those
+    #     of an fp32-dW fused plan bit for bit and dW_out == RNE(fp32 dW)
+    M, N, B = 520, 264, 24
+    X, dY = synth.factors(65, 0, rank, M, N, B, "int3", "int3")
+    W0, v0 = synth.sgd_state(65, 0, M, N)
+    Xd, dYd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(dY).to(torch.bfloat16).cuda()
+    pa = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "bf16", fuse_sgd=True, lr=1e-3, momentum=0.9,
+                     gather=gather)
+    pb = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", fuse_sgd=True, lr=1e-3, momentum=0.9,
+                     gather=gather)
+    Wa, va = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
+    Wb, vb = Wa.clone(), va.clone()
+    dWa = torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda")
+    dWb = torch.full((M, N), float("nan"), device="cuda")
+    for _ in range(2):
+        pa.sync_sgd(Xd, dYd, Wa, va, dWa)
+        pb.sync_sgd(Xd, dYd, Wb, vb, dWb)
+    torch.cuda.synchronize()
+    hashes = tdist.all_gather_object(digest(Wa) + digest(dWa))
+    record("fused_sgd_bf16_dw", torch.equal(Wa, Wb) and torch.equal(va, vb)
+           and torch.equal(dWa, dWb.to(torch.bfloat16)) and len(set(hashes)) == 1)
+    pa.close()
+    pb.close()
+
     # 8: a bucket (one push kernel + one reconstruction launch) == per-layer syncs, bit for bit
     specs = [(25088, 4096, 32, "relu", "masked_small"), (4096, 4096, 32, "relu", "masked_small"),
              (4096, 1000, 32, "relu", "softmax_onehot"), (520, 264, 24, "int3", "int3")]
     plans, Xs, dYs, refs, outs = [], [], [], [], []
     for li, (M, N, B, xd, dyd) in enumerate(specs):
         X, dY = synth.factors(2, 10 + li, rank, M, N, B, xd, dyd)
-        plans.append(tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32"))
+        plans.append(tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", gather=gather))
         Xs.append(torch.from_numpy(X).to(torch.bfloat16).cuda())
         dYs.append(torch.from_numpy(dY).to(torch.bfloat16).cuda())
         refs.append(torch.empty(M, N, device="cuda"))
@@ -184,11 +220,15 @@ def main():
 
     # 9: sharded reconstruction: each rank's rows == the same rows of the full dW, bit for bit,
     #    and the shards tile dW (fc6-sized factors, fused path; and an odd shape via the SIMT path)
+    #    (96 x 264 and 256 x 512: one and two 128-row tiles, so at n = 2 / 4 some ranks hold an
+    #    empty shard and still push their factors — the route is the same on every rank)
     for li, (M, N, B, xd, dyd, out_dt) in enumerate([(25088, 4096, 32, "relu", "masked_small", "f32"),
                                                      (1000, 264, 16, "int3", "int3", "bf16"),
-                                                     (130, 257, 5, "int3", "int3", "f32")]):
+                                                     (130, 257, 5, "int3", "int3", "f32"),
+                                                     (96, 264, 32, "int3", "int3", "f32"),
+                                                     (256, 512, 32, "int3", "int3", "f32")]):
         X, dY = synth.factors(3, 20 + li, rank, M, N, B, xd, dyd)
-        plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", out_dt)
+        plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", out_dt, gather=gather)
         Xd = torch.from_numpy(X).to(torch.bfloat16).cuda()
         dYd = torch.from_numpy(dY).to(torch.bfloat16).cuda()
         full = torch.empty(M, N, dtype=TDT[out_dt], device="cuda")
@@ -205,11 +245,12 @@ def main():
         plan.close()
 
     # 10: sharded bucket == the rows of per-layer full syncs
-    specs = [(25088, 4096, 32, "relu", "masked_small"), (4096, 1000, 32, "relu", "softmax_onehot")]
+    specs = [(25088, 4096, 32, "relu", "masked_small"), (4096, 1000, 32, "relu", "softmax_onehot"),
+             (96, 264, 32, "int3", "int3")]
     plans, Xs, dYs, fulls, shards = [], [], [], [], []
     for li, (M, N, B, xd, dyd) in enumerate(specs):
         X, dY = synth.factors(2, 30 + li, rank, M, N, B, xd, dyd)
-        p = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32")
+        p = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", gather=gather)
         plans.append(p)
         Xs.append(torch.from_numpy(X).to(torch.bfloat16).cuda())
         dYs.append(torch.from_numpy(dY).to(torch.bfloat16).cuda())
@@ -233,7 +274,7 @@ def main():
     plans, Xs, dYs, dWs = [], [], [], []
     for li, (M, N, B, xd, dyd) in enumerate(specs):
         X, dY = synth.factors(62, li, rank, M, N, B, xd, dyd)
-        plans.append(tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32"))
+        plans.append(tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", gather=gather))
         Xs.append(torch.from_numpy(X).to(torch.bfloat16).cuda())
         dYs.append(torch.from_numpy(dY).to(torch.bfloat16).cuda())
         dWs.append(torch.empty(M, N, device="cuda"))
@@ -260,7 +301,7 @@ def main():
     #     oracle's dense route, identical on every rank, for every choice of root
     M, N, B = 4096, 1000, 32
     X, dY = synth.factors(63, 0, rank, M, N, B, "relu", "softmax_onehot")
-    plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32")
+    plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", gather=gather)
     Xd, dYd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(dY).to(torch.bfloat16).cuda()
     Xall, dYall = synth.all_factors(63, 0, n, M, N, B, "relu", "softmax_onehot")
     Xe = torch.from_numpy(Xall).to(torch.bfloat16).double().numpy()

@@ -1,5 +1,6 @@
-"""Multi-GPU parity (n = 2 and 4) through torchrun + NCCL; skipped when the box has one GPU
-(the single-GPU virtual-n tests in test_gpu_recon.py cover the n-replica reconstruction)."""
+"""Multi-GPU parity (n = 2 and 4) through torchrun + NCCL; skipped when the box has one GPU (then
+tests/test_gpu_loopback.py runs the same code paths on a one-rank NCCL communicator and
+test_gpu_recon.py the n-replica reconstruction as virtual n)."""
 import json
 import os
 import socket
@@ -29,12 +30,11 @@ def test_multi_gpu_sfb(cuda, nproc, gather):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
            os.path.join(ROOT, "scripts", "multi_gpu_check.py")]
-    env = dict(os.environ)
     if gather == "nccl":
-        env["TAG_GATHER"] = "nccl"
+        cmd += ["--gather", "nccl"]
     if gather == "multicast":
-        env["TAG_MULTIMEM"] = "1"
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+        cmd += ["--multicast"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
     assert r.returncode == 0 and lines, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(lines[-1])
