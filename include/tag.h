@@ -152,7 +152,8 @@ typedef struct {
  *   AUTO: NVLink push into the peers' symmetric windows when every rank is NVLink load/store
  *         reachable and the factor rows are 16-byte multiples, else ncclAllGather;
  *   NCCL: always ncclAllGather (pack first when casting) — the library-collective baseline;
- *   PUSH: the NVLink push or TAG_ERR_UNSUPPORTED from tag_sfb_plan. */
+ *   PUSH: the NVLink push or TAG_ERR_UNSUPPORTED from tag_sfb_plan.
+ * Ignored on a one-rank comm without NCCL (TAG_GATHER_NONE: nothing is exchanged). */
 typedef enum {
     TAG_GATHER_REQ_AUTO = 0,
     TAG_GATHER_REQ_NCCL = 1,
