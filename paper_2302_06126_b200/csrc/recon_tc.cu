@@ -219,9 +219,24 @@ __device__ __forceinline__ void* mc_ptr(char* mc_base, ncclWindow_t w, size_t of
     return mc_base + static_cast<size_t>(w->mcOffset4K) * 4096 + off;
 }
 
+#if EXP_FUSED_DBG == 3
+// diagnostics builds: per-CTA %globaltimer stamps [cta][slot] — 0 start, 1 push stores issued,
+// 2 CTA barrier, 3 system-scope fence, 4 local counter add, 5 (last CTA of the rank) second fence +
+// remote adds, 6 first arrival wait satisfied, 7 end — printed by the host after each launch
+constexpr int DBG_SLOTS = 8;
+__device__ unsigned long long g_dbg_stamps[160 * DBG_SLOTS];
+#define DBG_STAMP(slot) (g_dbg_stamps[blockIdx.x * DBG_SLOTS + (slot)] = gtimer())
+#else
+#define DBG_STAMP(slot) ((void)0)
+#endif
+
 __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, int me) {
+    if (threadIdx.x == 0) DBG_STAMP(0);
     const int64_t G = gridDim.x;
-    constexpr int U = 4;                  // 16-byte loads in flight per thread before the stores
+#ifndef EXP_PUSH_U
+#define EXP_PUSH_U 4
+#endif
+    constexpr int U = EXP_PUSH_U;         // 16-byte loads in flight per thread before the stores
     char* const mc = gp.mc_base;
     for (int li = 0; li < gp.count; ++li) {
         const LayerParams& L = gp.L[li];
@@ -269,13 +284,17 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
     // CTA of this rank to arrive adds 1 to every layer's arrival counter on every peer, so each
     // counter sees n remote atomics per call (not n * grid) and its target does not depend on
     // the grid size (ranks may launch different grids, e.g. sharded with uneven shards).
+    if (threadIdx.x == 0) DBG_STAMP(1);
     __syncthreads();
     if (threadIdx.x == 0) {
+        DBG_STAMP(2);
         asm volatile("fence.acq_rel.sys;" ::: "memory");
+        DBG_STAMP(3);
         {
             uint32_t old;
             asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
                          : "=r"(old) : "l"(gp.local_ctr) : "memory");
+            DBG_STAMP(4);
             if (old + 1 != gp.local_target) return;        // not the last CTA of this rank
             // every other CTA's slice was released at system scope before its local add,
             // which this acquire observed; make that cumulative for the peers
@@ -293,6 +312,7 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
                 }
             }
         }
+        DBG_STAMP(5);
     }
 }
 
@@ -368,12 +388,9 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
     // no global memory is touched before the previous grid in the stream has completed
     grid_dep_wait();
     // Diagnostics builds only (scripts/build_variant.sh -DEXP_FUSED_DBG=k, never the product):
-    // 1 = no push and no wait, 2 = push without the arrival wait, 3 = printf phase stamps.
-    uint64_t t_start = 0, t_pushed = 0;
+    // 1 = no push and no wait, 2 = push without the arrival wait, 3 = phase stamps.
     if constexpr (FUSED) {
-        if (EXP_FUSED_DBG == 3) t_start = gtimer();
         if (EXP_FUSED_DBG != 1) fused_push(gp, npeers, me);
-        if (EXP_FUSED_DBG == 3) t_pushed = gtimer();
     }
 
     if (warp == 0) {
@@ -387,12 +404,7 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                 if constexpr (FUSED) {
                     if (!(ready & (1u << tr.li))) {
                         if (EXP_FUSED_DBG == 0 || EXP_FUSED_DBG == 3) fused_wait(gp.L[tr.li], me);
-#if EXP_FUSED_DBG == 3   // profiling builds only: a printf in the kernel costs 1-2 us per launch
-                        if (ready == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1))
-                            printf("fused rank %d cta %d push %llu ns, wait-after-push %llu ns\n", me,
-                                   blockIdx.x, (unsigned long long)(t_pushed - t_start),
-                                   (unsigned long long)(gtimer() - t_pushed));
-#endif
+                        if (ready == 0) DBG_STAMP(6);
                         ready |= 1u << tr.li;
                     }
                 }
@@ -840,6 +852,7 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
     if constexpr (CTAS == 2) ptx::cluster_sync();   // the leader's MMAs into the peer are done
     else __syncthreads();
     ptx::tc_fence_after();
+    if (FUSED && threadIdx.x == 0) DBG_STAMP(7);
     if (warp == 1) {
         if constexpr (CTAS == 2) ptx::tmem_dealloc_cg2<TMEM_COLS>(tmem_base);
         else ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
@@ -1038,8 +1051,40 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     cfg.attrs = attr;
     cfg.numAttrs = CTAS == 2 ? 2 : 1;
     const int npeers = FUSED ? fg->npeers : 1, me = FUSED ? fg->me : 0;
+#if EXP_FUSED_DBG == 3
+    if (FUSED) {
+        static unsigned long long zero[160 * DBG_SLOTS];
+        cudaMemcpyToSymbolAsync(g_dbg_stamps, zero, sizeof zero, 0, cudaMemcpyHostToDevice, s);
+    }
+#endif
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, gp, npeers, me);
     if (e != cudaSuccess) return cuda_fail(e, "launch recon_tc_kernel");
+#if EXP_FUSED_DBG == 3
+    if (FUSED) {
+        // diagnostics builds: phase stamps (max over CTAs, us from the earliest CTA start)
+        static unsigned long long st[160 * DBG_SLOTS];
+        cudaStreamSynchronize(s);
+        cudaMemcpyFromSymbol(st, g_dbg_stamps, sizeof st);
+        const int G = static_cast<int>(cfg.gridDim.x);
+        unsigned long long t0 = ~0ull;
+        for (int b = 0; b < G; ++b)
+            if (st[b * DBG_SLOTS] && st[b * DBG_SLOTS] < t0) t0 = st[b * DBG_SLOTS];
+        double mx[DBG_SLOTS] = {0}, mn[DBG_SLOTS];
+        for (int k = 0; k < DBG_SLOTS; ++k) mn[k] = 1e30;
+        for (int b = 0; b < G; ++b)
+            for (int k = 0; k < DBG_SLOTS; ++k)
+                if (st[b * DBG_SLOTS + k]) {
+                    const double v = (st[b * DBG_SLOTS + k] - t0) / 1000.0;
+                    mx[k] = v > mx[k] ? v : mx[k];
+                    mn[k] = v < mn[k] ? v : mn[k];
+                }
+        std::fprintf(stderr, "[fused dbg] rank %d grid %d us (min..max over CTAs): start %.1f..%.1f "
+                     "stores_issued %.1f..%.1f cta_barrier %.1f..%.1f sys_fence %.1f..%.1f "
+                     "local_add %.1f..%.1f publish(last CTA) %.1f wait_done %.1f..%.1f end %.1f..%.1f\n",
+                     fg->me, G, mn[0], mx[0], mn[1], mx[1], mn[2], mx[2], mn[3], mx[3], mn[4], mx[4],
+                     mx[5], mn[6], mx[6], mn[7], mx[7]);
+    }
+#endif
     count_launch();
     return TAG_OK;
 }

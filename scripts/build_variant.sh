@@ -1,18 +1,25 @@
 #!/bin/bash
-# Build an experimental libtag variant with extra nvcc defines for recon_tc.cu:
-#   scripts/build_variant.sh <name> -DSTAGES_PAIR=9 ...   -> build_exp/libtag_<name>.so
+# Build a diagnostics variant of libtag with extra nvcc defines (the EXP_* knobs of recon_tc.cu,
+# api.cu, push_gather.cu — e.g. -DEXP_FUSED_DBG=3, -DEXP_NO_FUSE=1, -DEXP_RECON_BN=256, -DEXP_R0=4):
+#   scripts/build_variant.sh <name> -DEXP_...=...   -> build_exp/libtag_<name>.so
 # Load it with TAG_LIB_PATH=build_exp/libtag_<name>.so (sweeps only; never the product path).
+# The product build (make -C paper_2302_06126_b200/csrc) sets none of these.
 set -e
 name=$1; shift
 root=$(cd "$(dirname "$0")/.." && pwd)
 csrc=$root/paper_2302_06126_b200/csrc
-nccl=/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl
-mkdir -p "$root/build_exp"
-make -C "$csrc" -s
-nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC,-fvisibility=hidden \
-  --expt-relaxed-constexpr -I$nccl/include -I$root/include -I$csrc "$@" -c "${SRC:-$csrc/recon_tc.cu}" -o "$root/build_exp/recon_tc_$name.o"
+nccl=${NCCL_HOME:-/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl}
+out=$root/build_exp/$name
+mkdir -p "$out"
+make -C "$csrc" -s NCCL_HOME=$nccl
 objs=""
-for o in api recon_simt pack_sgd push_gather bias select ilp; do objs="$objs $csrc/$o.o"; done
+for f in api recon_tc recon_simt pack_sgd push_gather bias; do
+  nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo -Xcompiler -fPIC,-fvisibility=hidden \
+    --expt-relaxed-constexpr -I$nccl/include -I$root/include -I$csrc "$@" -c "$csrc/$f.cu" -o "$out/$f.o" &
+  objs="$objs $out/$f.o"
+done
+wait
+objs="$objs $csrc/select.o $csrc/ilp.o"
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o "$root/build_exp/libtag_$name.so" $objs \
-  "$root/build_exp/recon_tc_$name.o" -cudart static -L$nccl/lib -l:libnccl.so.2 -Xlinker -rpath,$nccl/lib
+  -cudart static -L$nccl/lib -l:libnccl.so.2 -Xlinker -rpath,$nccl/lib
 echo "built build_exp/libtag_$name.so"

@@ -1,7 +1,9 @@
 #!/usr/bin/env python3
 """Fused push+reconstruction timing probe (torchrun): the VGG-19 bucket, cold (L2 flushed, ranks
-aligned by tag_comm_barrier), CUDA events around one tag_sfb_group_sync. TAG_FUSED_DEBUG=1/2/3
-select the profiling variants of the fused kernel (no push / no wait / printf stamps)."""
+aligned by tag_comm_barrier), CUDA events around one tag_sfb_group_sync. Diagnostics variants of
+the library (scripts/build_variant.sh, loaded with TAG_LIB_PATH) select the profiling forms of the
+fused kernel (no push / no wait / printf stamps); --label names the variant in the output."""
+import argparse
 import json
 import os
 import statistics
@@ -13,13 +15,17 @@ import torch  # noqa: E402
 from paper_2302_06126_b200 import dist as tdist  # noqa: E402
 from paper_2302_06126_b200 import synth, tag  # noqa: E402
 
+ap = argparse.ArgumentParser()
+ap.add_argument("--label", default="product")
+ap.add_argument("--gather", default="auto")
+args = ap.parse_args()
 rank, local_rank, world = tdist.init_from_env()
 torch.cuda.set_device(local_rank)
 comm = tdist.bootstrap_comm(tag, local_rank)
 cfg = synth.CONFIGS[2]
 plans, Xs, dYs, dWs = [], [], [], []
 for li, L in enumerate(cfg.layers):
-    plans.append(tag.SfbPlan(comm, L.M, L.N, L.B))
+    plans.append(tag.SfbPlan(comm, L.M, L.N, L.B, gather=args.gather))
     Xs.append(torch.randn(L.B, L.M, device="cuda").to(torch.bfloat16))
     dYs.append(torch.randn(L.B, L.N, device="cuda").to(torch.bfloat16))
     dWs.append(torch.empty(L.M, L.N, device="cuda"))
@@ -44,9 +50,12 @@ for it in range(iters + 3):
     if it >= 3:
         ts.append(e0.elapsed_time(e1))
 t = tdist.max_over_ranks(statistics.median(ts))
+p10 = tdist.max_over_ranks(sorted(ts)[len(ts) // 10])
 if rank == 0:
-    print(json.dumps({"n": world, "dbg": os.environ.get("TAG_FUSED_DEBUG", "0"),
-                      "no_fuse": bool(os.environ.get("TAG_NO_FUSE")), "step_us": round(t * 1e3, 2)}),
+    print(json.dumps({"n": world, "variant": args.label, "gather": args.gather,
+                      "lib": os.environ.get("TAG_LIB_PATH", "libtag.so"),
+                      "step_us": round(t * 1e3, 2),
+                      "p10_us": round(p10 * 1e3, 2)}),
           flush=True)
 g.close()
 for p in plans:
