@@ -102,29 +102,54 @@ class ClockSampler:
                 "samples": len(rows)}
 
 
-def cpu_oracle_baseline(cfg, n, budget_mac=2.5e10):
-    """Time the fp64 CPU oracle (as it stands) on a bounded sample of the same workload: the first
-    M_s input-feature rows of every layer's dW, M_s scaled so the sample is ~budget_mac MACs."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_oracle_baseline(cfg, n, budget_mac=1.25e10, reps=3):
+    """Time the fp64 CPU oracle (as it stands) on a bounded sample of the same workload, SURVEY
+    d-5: both routes — the dense route (per-replica products summed in rank order) and
+    the SFB route (rank-1 outer-product accumulation) — on the first M_s input-feature
+    rows of every layer's dW, M_s scaled so each route is ~budget_mac MACs; median of `reps` runs
+    per route; the reported value is the SFB route's dW GB/s (the dense route's beside it)."""
     import oracle
     oracle.build()
     cores = os.cpu_count()
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    total_bytes, total_t, desc = 0, 0.0, []
     full_mac = sum(L.M * L.N * n * L.B for L in cfg.layers)
     frac = min(1.0, budget_mac / full_mac)
+    samples, desc, out_bytes = [], [], 0
     for li, L in enumerate(cfg.layers):
         Ms = max(8, int(L.M * frac))
         X, dY = synth.all_factors(cfg.cid, li, n, L.M, L.N, L.B, L.x_dist, L.dy_dist)
         Xs = torch.from_numpy(np.ascontiguousarray(X[:, :, :Ms])).to(torch.bfloat16).double().numpy()
         dYe = torch.from_numpy(dY).to(torch.bfloat16).double().numpy()
-        t0 = time.perf_counter()
-        oracle.sfb_dw(Xs, dYe)
-        total_t += time.perf_counter() - t0
-        total_bytes += Ms * L.N * ESIZE[cfg.out_dtype]
+        samples.append((Xs, dYe))
+        out_bytes += Ms * L.N * ESIZE[cfg.out_dtype]
         desc.append(f"{L.name}:{Ms}/{L.M} rows")
-    return {"value": total_bytes / total_t / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
-            "seconds": round(total_t, 3),
-            "sample": f"fp64 SFB route, n={n}, K={n * cfg.layers[0].B}, dW rows " + ", ".join(desc)}
+    secs = {}
+    for route, fn in (("sfb", oracle.sfb_dw), ("dense", oracle.dense_dw)):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            for Xs, dYe in samples:
+                fn(Xs, dYe)
+            ts.append(time.perf_counter() - t0)
+        secs[route] = statistics.median(ts)
+    return {"value": out_bytes / secs["sfb"] / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(), "seconds": round(secs["sfb"], 3),
+            "dense_route": {"value": out_bytes / secs["dense"] / 1e9, "unit": "GB/s",
+                            "seconds": round(secs["dense"], 3)},
+            "stat": f"median of {reps} per route",
+            "sample": f"fp64 SFB and dense routes, n={n}, K={n * cfg.layers[0].B}, dW rows "
+                      + ", ".join(desc)}
 
 
 def run_reference(args, cfg, rank, world):
@@ -135,7 +160,7 @@ def run_reference(args, cfg, rank, world):
     vals, secs = [], []
     cb = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_oracle_baseline(cfg, n, budget_mac=args.ref_mac)
+        cb = cpu_oracle_baseline(cfg, n, budget_mac=args.ref_mac, reps=1)
         if i >= args.warmup:
             vals.append(cb["value"])
             secs.append(cb["seconds"])
@@ -240,7 +265,8 @@ def config_json(cfg, n, args):
             "layers": [f"{L.name} {L.M}x{L.N}" for L in cfg.layers], "rows_per_gpu": cfg.layers[0].B,
             "n": n, "in/wire/out": f"{cfg.in_dtype}/{cfg.wire_dtype}/{cfg.out_dtype}",
             "parallelism": f"dp{n} (SFB all-gather + replicated reconstruction)",
-            "l2": "flushed between timed steps (256 MiB write + 256 MiB read), outside the timed interval"}
+            "l2": "flushed between timed steps (256 MiB write + 256 MiB read), outside the timed interval",
+            "nccl_algo": os.environ.get("NCCL_ALGO", "default")}
 
 
 def main():
@@ -254,11 +280,15 @@ def main():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--ref-mac", type=float, default=2.5e10)
     ap.add_argument("--no-virtual", action="store_true")
+    ap.add_argument("--nccl-algo", default=None,
+                    help="set NCCL_ALGO (e.g. ring) for this run, before any communicator exists")
     ap.add_argument("--per-layer-step", action="store_true",
                     help="time the step as one tag_sfb_sync per layer instead of one bucket")
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "need >= 3 warm-up steps"
 
+    if args.nccl_algo:
+        os.environ["NCCL_ALGO"] = args.nccl_algo
     rank, local_rank, world = tdist.init_from_env()
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":
@@ -292,12 +322,24 @@ def main():
                          int(peaks.get("bf16_tflops_sustained", 1400) * 1e12))
     # profiled selector (paper's profiler P:331-334): curves measured by scripts/profile_comm.py
     choices_prof = None
+    profiled_compute = None
     prof_path = os.path.join(ROOT, "profiles", f"comm_n{n}.json")
     if n > 1 and os.path.exists(prof_path):
         prof = json.load(open(prof_path))
+        # measured op times (scripts/profile_compute.py, the paper's op profiler P:323-329)
+        # replace the linear compute model when this config and n were profiled
+        rec = loc = None
+        cp = os.path.join(ROOT, "profiles", "compute_profile.json")
+        if os.path.exists(cp):
+            ct = json.load(open(cp)).get(str(args.config), {})
+            if all(str(n) in ct.get(l["L"].name, {}) for l in layers):
+                rec = [ct[l["L"].name][str(n)]["recon_ns"] for l in layers]
+                loc = [ct[l["L"].name][str(n)]["local_ns"] for l in layers]
         choices_prof = tag.select_profiled(sel_layers, n, prof["gather"], prof["allreduce"],
                                            int(peaks.get("bf16_tflops_sustained", 1400) * 1e12),
-                                           prof.get("ps"))
+                                           prof.get("ps"), recon_ns=rec, local_ns=loc)
+        profiled_compute = "measured op times (profiles/compute_profile.json)" if rec else \
+            "linear model 2MNB/F"
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     flush_rd = torch.ones(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
@@ -465,7 +507,8 @@ def main():
         ag = (n - 1) * L.B * (L.M + L.N) * ESIZE[cfg.wire_dtype]
         per_layer[L.name] = {
             "sync_us": round(t_sync * 1e3, 2), "recon_us": round(t_rec * 1e3, 2),
-            "gather_us": round((t_sync - t_rec) * 1e3, 2),
+            # staged gather stage (a1 + a2; n = 1: no exchange, only the event gap)
+            ("gather_us" if n > 1 else "stage_gap_us"): round((t_sync - t_rec) * 1e3, 2),
             "dW_GBps": round(L.M * L.N * ESIZE[cfg.out_dtype] / (t_sync * 1e-3) / 1e9, 1),
             "recon_hbm_frac": round(rbytes / (t_rec * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
             "recon_tensor_frac": round(flops / (t_rec * 1e-3) / 1e12 / peaks["bf16_tflops"], 4),
@@ -483,34 +526,55 @@ def main():
                                       "frac_of_900": round(ag_all / (t_gather * 1e-3) / 900e9, 4)}
 
     # ---------------------------------------------------------------- dense baseline (n > 1)
+    # SURVEY d-1b: from (X_r, dY_r) to the synchronised result on every rank. Dense = local GEMM
+    # (K = B) + ncclAllReduce with PreMulSum(1/(nB)) (+ the unfused SGD step for E2 configs, whose
+    # SFB side fuses it). The AllReduce alone is timed too and reported as nccl-tests bus
+    # bandwidth 2(n-1)/n * M*N*e_g / t against 900 GB/s and as a fraction of the ring ideal
+    # 2(n-1)/n * G / 900 GB/s. NCCL picks its algorithm unless the run sets
+    # NCCL_ALGO (bench --nccl-algo ring), which `nccl_algo` in the config records.
     if n > 1 and not args.no_dense:
-        for i, l in enumerate(layers):
-            L = l["L"]
+        reps = max(3, min(args.steps, 10))
+
+        def timed(fn):
             t = []
-            for _ in range(max(3, min(args.steps, 10))):
+            for _ in range(reps):
                 e0, e1 = start_events(2)
-                l["plan"].local_grad(l["X"], l["dY"], l["dW"], stream)
-                l["plan"].dense_allreduce(l["dW"], stream)
+                with torch.cuda.stream(stream):
+                    fn()
                 e1.record(stream)
                 torch.cuda.synchronize()
                 t.append(e0.elapsed_time(e1))
-            td = tdist.max_over_ranks(statistics.median(t))
+            return tdist.max_over_ranks(statistics.median(t))
+        for i, l in enumerate(layers):
+            L, plan = l["L"], l["plan"]
+
+            def dense():
+                plan.local_grad(l["X"], l["dY"], l["dW"], stream)
+                plan.dense_allreduce(l["dW"], stream)
+                if cfg.sgd:
+                    plan.sgd_step(l["dW"], l["W"], l["v"], stream)
+            td = timed(dense)
+            ta = timed(lambda: plan.dense_allreduce(l["dW"], stream))
             # Replicate-with-PS: the same local gradient, reduced to a round-robin PS
             # (root = layer index mod n) and broadcast back
-            t = []
-            for _ in range(max(3, min(args.steps, 10))):
-                e0, e1 = start_events(2)
-                l["plan"].local_grad(l["X"], l["dY"], l["dW"], stream)
-                l["plan"].ps_sync(l["dW"], i % n, stream)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                t.append(e0.elapsed_time(e1))
-            tp = tdist.max_over_ranks(statistics.median(t))
-            per_layer[L.name]["dense_us"] = round(td * 1e3, 2)
-            per_layer[L.name]["ps_us"] = round(tp * 1e3, 2)
-            per_layer[L.name]["sfb_speedup_vs_dense"] = round(td / (per_layer[L.name]["sync_us"] / 1e3), 2)
-            per_layer[L.name]["measured_winner"] = min(
-                [(per_layer[L.name]["sync_us"], "sfb"), (td * 1e3, "allreduce"), (tp * 1e3, "ps")])[1]
+            tp = timed(lambda: (plan.local_grad(l["X"], l["dY"], l["dW"], stream),
+                                plan.ps_sync(l["dW"], i % n, stream)))
+            G = L.M * L.N * ESIZE[cfg.out_dtype]
+            ring_ideal_us = 2 * (n - 1) / n * G / 900e9 * 1e6
+            pl = per_layer[L.name]
+            pl["dense_us"] = round(td * 1e3, 2)
+            pl["dense_includes_sgd_step"] = bool(cfg.sgd)
+            pl["allreduce_us"] = round(ta * 1e3, 2)
+            pl["allreduce_busbw_GBps"] = round(2 * (n - 1) / n * G / (ta * 1e-3) / 1e9, 1)
+            pl["allreduce_frac_of_900"] = round(2 * (n - 1) / n * G / (ta * 1e-3) / 900e9, 4)
+            pl["allreduce_frac_of_ring_ideal"] = round(ring_ideal_us / (ta * 1e3), 4)
+            pl["ps_us"] = round(tp * 1e3, 2)
+            pl["sfb_speedup_vs_dense"] = round(td / (pl["sync_us"] / 1e3), 2)
+            pl["measured_winner"] = min([(pl["sync_us"], "sfb"), (td * 1e3, "allreduce"),
+                                         (tp * 1e3, "ps")])[1]
+            pl["selector_agrees"] = pl["selector"] == pl["measured_winner"]
+            pl["selector_profiled_agrees"] = (pl["selector_profiled"] == pl["measured_winner"]
+                                              if pl["selector_profiled"] else None)
 
     # ---------------------------------------------------------------- sharded variant (n > 1)
     # every rank still receives all factors but reconstructs only its
@@ -592,7 +656,7 @@ def main():
                 "per_layer": per_layer, "roofline": roofline, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu,
                 "virtual_n8_recon": virt, "projected_n8": proj8, "step_stats": step_stats,
-                "sharded_variant": sharded,
+                "sharded_variant": sharded, "selector_profiled_compute": profiled_compute,
                 "lib": tag.version()}
         print(json.dumps(line), flush=True)
     if group is not None:

@@ -371,7 +371,15 @@ tag_status_t tag_sfb_select(const tag_layer_t* layers, int num_layers, const tag
  * "Replicate with PS"), PS is chosen iff ps(G) is strictly below both other costs
  * (ties: AllReduce, then SFB). Exact integer arithmetic (bit-identical on every rank and
  * to oracle/selector.py). Limits (TAG_ERR_INVALID_ARG beyond): n <= 65536, M, N, B <= 2^24,
- * curve ns <= 2^40, bytes <= 2^62. */
+ * curve ns <= 2^40, bytes <= 2^62.
+ * Measured op times (the paper profiles every op at the batch size, instead of the
+ * linear model P:326-328): when recon_ns and local_ns are both non-NULL, recon_ns[i] is the
+ * measured time of layer i's reconstruction at K = nB (tag_sfb_reconstruct) and local_ns[i] that
+ * of the dense path's local gradient at K = B (tag_local_grad), e.g. from
+ * scripts/profile_compute.py, and the costs become
+ *   SFB = gather((n-1) S) + recon_ns[i],  AllReduce = local_ns[i] + allreduce(G),
+ *   PS  = local_ns[i] + ps(G)
+ * (same tie rule; tensor_flops is then ignored). Each value <= 2^40. */
 typedef struct {
     int count;
     const uint64_t* bytes;
@@ -383,6 +391,8 @@ typedef struct {
     tag_curve_t allreduce;   /* x = gradient bytes M N e_g */
     uint64_t tensor_flops;   /* F; 0 drops the compute term */
     tag_curve_t ps;          /* x = gradient bytes M N e_g (tag_ps_sync); count 0: no PS option */
+    const uint64_t* recon_ns;  /* [num_layers] measured reconstruction ns at K = nB, or NULL */
+    const uint64_t* local_ns;  /* [num_layers] measured local-gradient ns at K = B, or NULL  */
 } tag_profiled_topology_t;
 tag_status_t tag_sfb_select_profiled(const tag_layer_t* layers, int num_layers,
                                      const tag_profiled_topology_t* topo, tag_choice_t* out);

@@ -138,21 +138,28 @@ def curve_ns(points, x):
     return max(t, 0)
 
 
-def select_profiled(layer, n, gather_pts, allreduce_pts, F=0, ps_pts=None):
+def select_profiled(layer, n, gather_pts, allreduce_pts, F=0, ps_pts=None, recon_ns=None,
+                    local_ns=None):
     """SFB iff gather((n-1) S) + floor((n-1) 2MNB 1e9 / F) < allreduce(G); ties -> AllReduce.
     With a PS curve ("Replicate with PS"): PS iff ps(G) is strictly below both
-    (ties: AllReduce, then SFB)."""
+    (ties: AllReduce, then SFB). With measured op times (the paper's profiler) the
+    compute term is the measured one: SFB = gather + recon_ns, AllReduce = local_ns + ar(G),
+    PS = local_ns + ps(G)."""
     if n <= 1:
         return CHOICE_NONE
     M, N, B, e_w, e_g = layer["M"], layer["N"], layer["B"], layer["e_w"], layer["e_g"]
     S = B * (M + N) * e_w
     G = M * N * e_g
     t_sfb = curve_ns(gather_pts, (n - 1) * S)
-    if F:
+    t_local = 0
+    if recon_ns is not None:
+        t_sfb += recon_ns
+        t_local = local_ns
+    elif F:
         t_sfb += ((n - 1) * 2 * M * N * B * 10 ** 9) // F
-    costs = [(curve_ns(allreduce_pts, G), 0, CHOICE_ALLREDUCE), (t_sfb, 1, CHOICE_SFB)]
+    costs = [(t_local + curve_ns(allreduce_pts, G), 0, CHOICE_ALLREDUCE), (t_sfb, 1, CHOICE_SFB)]
     if ps_pts:
-        costs.append((curve_ns(ps_pts, G), 2, CHOICE_PS))
+        costs.append((t_local + curve_ns(ps_pts, G), 2, CHOICE_PS))
     return min(costs)[2]
 
 

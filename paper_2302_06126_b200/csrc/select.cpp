@@ -159,6 +159,14 @@ extern "C" tag_status_t tag_sfb_select_profiled(const tag_layer_t* layers, int n
             (L.grad_dtype != TAG_F32 && L.grad_dtype != TAG_BF16))
             return fail(TAG_ERR_INVALID_ARG, "tag_sfb_select_profiled: unknown dtype");
     }
+    const bool measured = topo->recon_ns != nullptr && topo->local_ns != nullptr;
+    if ((topo->recon_ns != nullptr) != (topo->local_ns != nullptr))
+        return fail(TAG_ERR_INVALID_ARG,
+                    "tag_sfb_select_profiled: recon_ns and local_ns go together");
+    if (measured)
+        for (int i = 0; i < num_layers; ++i)
+            if (topo->recon_ns[i] > (1ull << 40) || topo->local_ns[i] > (1ull << 40))
+                return fail(TAG_ERR_INVALID_ARG, "tag_sfb_select_profiled: op time above 2^40 ns");
     const i128 n = topo->n;
     const i128 F = static_cast<i128>(topo->tensor_flops);
     for (int i = 0; i < num_layers; ++i) {
@@ -171,13 +179,22 @@ extern "C" tag_status_t tag_sfb_select_profiled(const tag_layer_t* layers, int n
         const i128 S = B * (M + N) * static_cast<i128>(dtype_size(L.factor_dtype));
         const i128 G = M * N * static_cast<i128>(dtype_size(L.grad_dtype));
         i128 t_sfb = curve_ns(topo->gather, (n - 1) * S);
-        if (F > 0) t_sfb += floor_div((n - 1) * 2 * M * N * B * 1000000000, F);
-        const i128 t_ar = curve_ns(topo->allreduce, G);
+        i128 t_ar = curve_ns(topo->allreduce, G);
+        i128 t_local = 0;
+        if (measured) {
+            // the measured ops: SFB reconstructs at K = nB, the dense paths compute
+            // the local gradient at K = B before their collective
+            t_sfb += static_cast<i128>(topo->recon_ns[i]);
+            t_local = static_cast<i128>(topo->local_ns[i]);
+            t_ar += t_local;
+        } else if (F > 0) {
+            t_sfb += floor_div((n - 1) * 2 * M * N * B * 1000000000, F);
+        }
         // AllReduce unless strictly beaten; then SFB; then PS if strictly below the best so far
         tag_choice_t c = TAG_SYNC_ALLREDUCE;
         i128 best = t_ar;
         if (t_sfb < best) { c = TAG_SYNC_SFB; best = t_sfb; }
-        if (has_ps && curve_ns(topo->ps, G) < best) c = TAG_SYNC_PS;
+        if (has_ps && t_local + curve_ns(topo->ps, G) < best) c = TAG_SYNC_PS;
         out[i] = c;
     }
     return TAG_OK;

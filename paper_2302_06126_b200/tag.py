@@ -64,7 +64,9 @@ class Curve(ctypes.Structure):
 
 class ProfiledTopology(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int), ("gather", Curve), ("allreduce", Curve),
-                ("tensor_flops", ctypes.c_uint64), ("ps", Curve)]
+                ("tensor_flops", ctypes.c_uint64), ("ps", Curve),
+                ("recon_ns", ctypes.POINTER(ctypes.c_uint64)),
+                ("local_ns", ctypes.POINTER(ctypes.c_uint64))]
 
 
 class IlpInstance(ctypes.Structure):
@@ -458,9 +460,11 @@ def _curve(points):
     return Curve(len(pts), b, t), (b, t)
 
 
-def select_profiled(layers, n, gather_points, allreduce_points, tensor_flops=0, ps_points=None):
+def select_profiled(layers, n, gather_points, allreduce_points, tensor_flops=0, ps_points=None,
+                    recon_ns=None, local_ns=None):
     """Per-layer choice from measured cost curves [(bytes, ns), ...] (tag_sfb_select_profiled);
-    ps_points (optional) adds the Replicate-with-PS option (SYNC_PS)."""
+    ps_points (optional) adds the Replicate-with-PS option (SYNC_PS); recon_ns / local_ns
+    (optional, per layer) are measured op times replacing the tensor_flops model."""
     layers = list(layers)
     arr = (LayerDesc * max(1, len(layers)))()
     for i, L in enumerate(layers):
@@ -472,11 +476,18 @@ def select_profiled(layers, n, gather_points, allreduce_points, tensor_flops=0, 
         ps, keep_p = _curve(ps_points)
     else:
         ps, keep_p = Curve(0, None, None), None
-    topo = ProfiledTopology(n, g, a, tensor_flops, ps)
+    rn = ln = None
+    if recon_ns is not None or local_ns is not None:
+        assert recon_ns is not None and local_ns is not None and len(recon_ns) == len(local_ns) == len(layers)
+        rn = (ctypes.c_uint64 * max(1, len(layers)))(*[int(x) for x in recon_ns])
+        ln = (ctypes.c_uint64 * max(1, len(layers)))(*[int(x) for x in local_ns])
+    topo = ProfiledTopology(n, g, a, tensor_flops, ps,
+                            ctypes.cast(rn, ctypes.POINTER(ctypes.c_uint64)) if rn else None,
+                            ctypes.cast(ln, ctypes.POINTER(ctypes.c_uint64)) if ln else None)
     out = (ctypes.c_int * max(1, len(layers)))()
     _check(_lib.tag_sfb_select_profiled(arr, len(layers), ctypes.byref(topo), out),
            "tag_sfb_select_profiled")
-    del keep_g, keep_a, keep_p
+    del keep_g, keep_a, keep_p, rn, ln
     return [out[i] for i in range(len(layers))]
 
 

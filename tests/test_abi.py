@@ -143,6 +143,37 @@ def test_select_profiled_bit_exact(tagmod, oracle_mod):
         assert got == want
 
 
+def test_select_profiled_measured_times_bit_exact(tagmod, oracle_mod):
+    """f-4: measured per-layer op times (recon at K = nB, local gradient at K = B) in the profiled
+    selector, library == oracle, with and without the PS curve."""
+    S = oracle_mod.selector
+    rs = np.random.default_rng(37)
+    dt = {2: "bf16", 4: "f32"}
+    seen = set()
+    for _ in range(300):
+        def curve():
+            b = np.cumsum(rs.integers(1, 10 ** 8, int(rs.integers(2, 6)))).tolist()
+            return list(zip(b, rs.integers(1000, 10 ** 7, len(b)).tolist()))
+        g, a, ps = curve(), curve(), (curve() if rs.integers(0, 2) else None)
+        n = int(rs.integers(1, 9))
+        lays = [dict(M=int(rs.integers(1, 30000)), N=int(rs.integers(1, 30000)),
+                     B=int(rs.integers(1, 2048)), e_w=int(rs.choice([2, 4])),
+                     e_g=int(rs.choice([2, 4]))) for _ in range(4)]
+        rec = [int(rs.integers(0, 10 ** 7)) for _ in lays]
+        loc = [int(rs.integers(0, 10 ** 6)) for _ in lays]
+        got = tagmod.select_profiled([dict(M=l["M"], N=l["N"], B=l["B"], factor_dtype=dt[l["e_w"]],
+                                           grad_dtype=dt[l["e_g"]]) for l in lays], n, g, a, 10 ** 15,
+                                     ps, recon_ns=rec, local_ns=loc)
+        want = [S.select_profiled(l, n, g, a, 10 ** 15, ps, recon_ns=r, local_ns=o)
+                for l, r, o in zip(lays, rec, loc)]
+        assert got == want
+        seen.update(got)
+    assert {tagmod.SYNC_ALLREDUCE, tagmod.SYNC_SFB, tagmod.SYNC_NONE} <= seen
+    with pytest.raises(tagmod.TagError):
+        tagmod.select_profiled([dict(M=4, N=4, B=1)], 2, [(1, 1), (2, 2)], [(1, 1), (2, 2)],
+                               recon_ns=[1 << 41], local_ns=[0])
+
+
 def test_select_profiled_errors(tagmod):
     with pytest.raises(tagmod.TagError):
         tagmod.select_profiled([dict(M=4, N=4, B=1)], 2, [(1, 1)], [(1, 1), (2, 2)])   # 1 point

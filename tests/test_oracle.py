@@ -206,6 +206,52 @@ def test_spec_ring_allreduce(oracle_mod):
         assert t == Fraction(c["seconds"])
 
 
+def _simulate_ring_allreduce(n, chunks):
+    """Independent brute force: a ring AllReduce of n ranks' vectors, each split into n chunks —
+    reduce-scatter (n-1 steps: rank r sends its running sum of chunk (r - s) mod n to r+1), then
+    all-gather (n-1 steps: the owner of a finished chunk passes it on). Returns (per-rank result,
+    elements each rank sent)."""
+    data = [[list(c) for c in chunks_r] for chunks_r in chunks]      # data[rank][chunk] = list
+    sent = [0] * n
+    for s in range(n - 1):                                           # reduce-scatter
+        msgs = []
+        for r in range(n):
+            c = (r - s) % n
+            msgs.append(((r + 1) % n, c, list(data[r][c])))
+            sent[r] += len(data[r][c])
+        for dst, c, vals in msgs:
+            data[dst][c] = [a + b for a, b in zip(data[dst][c], vals)]
+    for s in range(n - 1):                                           # all-gather
+        msgs = []
+        for r in range(n):
+            c = (r + 1 - s) % n
+            msgs.append(((r + 1) % n, c, list(data[r][c])))
+            sent[r] += len(data[r][c])
+        for dst, c, vals in msgs:
+            data[dst][c] = vals
+    return data, sent
+
+
+def test_ring_allreduce_bytes_brute_force(oracle_mod):
+    """ring_allreduce_bytes (P:566 / P:611-612: 2(D-1)/D * L per rank) against a simulated ring
+    that also checks the reduction itself; and its time equals ring_allreduce_time."""
+    S = oracle_mod.selector
+    rng = np.random.default_rng(7)
+    for n in (2, 3, 4, 8):
+        for M, N in ((4, 6), (8, 3), (5, 8)):
+            L = M * N * n                            # elements; divisible into n equal chunks
+            vecs = [rng.integers(-5, 5, L).tolist() for _ in range(n)]
+            chunks = [[v[c * (L // n):(c + 1) * (L // n)] for c in range(n)] for v in vecs]
+            data, sent = _simulate_ring_allreduce(n, chunks)
+            want = [sum(col) for col in zip(*vecs)]
+            for r in range(n):
+                assert sum(data[r], []) == want
+            for e_g in (2, 4):
+                assert all(Fraction(x * e_g) == S.ring_allreduce_bytes(n, M * n, N, e_g) for x in sent)
+                assert S.ring_allreduce_bytes(n, M * n, N, e_g) / Fraction(10 ** 9) == \
+                    S.ring_allreduce_time(n, M * n * N * e_g, 10 ** 9)
+
+
 def test_spec_ilp_objective(oracle_mod):
     S = oracle_mod.selector
     c1, c2 = _golden("spec_sfb_ilp.json")["cases"]
@@ -405,3 +451,35 @@ def test_adam_matches_torch_optim(oracle_mod):
         opt.step()
         W, m, v = oracle_mod.adam(g, W, m, v, 3e-3, 0.8, 0.95, 1e-6, 0.01, t)
         np.testing.assert_allclose(W, p.detach().numpy(), rtol=1e-12, atol=1e-14)
+
+
+def test_profiled_measured_op_times_reduce_to_linear_model(oracle_mod):
+    """Measured op times that follow the linear model — recon time =
+    local time + floor((n-1) 2MNB 1e9 / F) — give the analytic-compute decision exactly, with and
+    without the PS option, whatever the local time; a measured reconstruction slower than the
+    model by more than the margin flips SFB to AllReduce."""
+    S = oracle_mod.selector
+    rs = np.random.default_rng(41)
+    flips = 0
+    for _ in range(2000):
+        def curve():
+            b = np.cumsum(rs.integers(1, 10 ** 8, int(rs.integers(2, 6)))).tolist()
+            return list(zip(b, rs.integers(1000, 10 ** 7, len(b)).tolist()))
+        g, a, ps = curve(), curve(), curve()
+        n = int(rs.integers(2, 9))
+        F = int(rs.integers(10 ** 12, 3 * 10 ** 15))
+        L = dict(M=int(rs.integers(1, 30000)), N=int(rs.integers(1, 30000)),
+                 B=int(rs.integers(1, 2048)), e_w=int(rs.choice([2, 4])), e_g=int(rs.choice([2, 4])))
+        extra = ((n - 1) * 2 * L["M"] * L["N"] * L["B"] * 10 ** 9) // F
+        local = int(rs.integers(0, 10 ** 6))
+        for p in (None, ps):
+            want = S.select_profiled(L, n, g, a, F, p)
+            assert S.select_profiled(L, n, g, a, 0, p, recon_ns=local + extra, local_ns=local) == want
+        if S.select_profiled(L, n, g, a, F) == S.CHOICE_SFB:
+            margin = S.curve_ns(a, L["M"] * L["N"] * L["e_g"]) - (
+                S.curve_ns(g, (n - 1) * L["B"] * (L["M"] + L["N"]) * L["e_w"]) + extra)
+            assert margin > 0
+            assert S.select_profiled(L, n, g, a, 0, None, recon_ns=local + extra + margin,
+                                     local_ns=local) == S.CHOICE_ALLREDUCE
+            flips += 1
+    assert flips > 100
