@@ -250,6 +250,22 @@ tag_status_t tag_sfb_shard_rows(tag_sfb_plan_t plan, int rank, int64_t* row_begi
 tag_status_t tag_sfb_sync_sharded(tag_sfb_plan_t plan, const void* X, const void* dY,
                                   void* dW_shard, tag_stream_t stream);
 
+/* COLLECTIVE (n > 1). Sharded optimizer step + parameter all-gather (ZeRO-style; SURVEY §8(f)
+ * rank 2; the Duplicate replicates the gradient op, and here the optimizer op l is
+ * sharded instead of replicated): every rank receives all factors (a1 + a2, fused push), rank r
+ * reconstructs only its rows [row_begin, row_begin + row_count) of dW (tag_sfb_shard_rows) and
+ * applies SGD-momentum to those rows of W and to its momentum shard in the same epilogue (dW is
+ * never stored), then the updated rows of W are all-gathered (one in-place ncclAllGather when
+ * the shards are equal, else one ncclBroadcast per shard) so every rank ends with the whole W.
+ * W: M x N fp32, the full parameter (read and written only in this rank's rows before the
+ * all-gather; every row is overwritten by its owner's result). v_shard: row_count x N fp32, this
+ * rank's momentum rows (may be NULL when row_count == 0). Requires desc.fuse_sgd = 1 and
+ * out_dtype F32. W after the call is bitwise equal to tag_sfb_sync_sgd's on every rank (the same
+ * per-row arithmetic), and v_shard to the same rows of its v. n = 1: one shard, no all-gather.
+ * Errors: TAG_ERR_INVALID_ARG (plan without fuse_sgd, NULL / misaligned pointers). */
+tag_status_t tag_sfb_sync_sharded_sgd(tag_sfb_plan_t plan, const void* X, const void* dY, float* W,
+                                      float* v_shard, tag_stream_t stream);
+
 /* Bias gradient of the layer (y = x W + b; DESIGN R17): db = alpha * sum_k dY_all[k][:], the
  * column sums of the gathered output gradients — the bias is the weight of a constant input, so
  * its gradient is the outer product of the ones vector with the factor dY that SFB already

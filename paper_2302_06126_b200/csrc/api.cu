@@ -853,6 +853,88 @@ tag_status_t tag_sfb_sync_sharded(tag_sfb_plan_t p, const void* X, const void* d
     return st;
 }
 
+// Parameter all-gather of the sharded optimizer step: rank r's rows [rb_r, rb_r + rc_r) of W
+// reach every rank. Equal shards: one in-place ncclAllGather; otherwise one ncclBroadcast per
+// non-empty shard in a group. n = 1 / no collective: nothing to do.
+tag_status_t allgather_rows(tag_plan_s* p, float* W, cudaStream_t s) {
+    tag_comm_s* c = p->comm;
+    if (!has_collective(c) || c->nranks == 1) return TAG_OK;
+    const int64_t N = p->d.N;
+    int64_t rb0, rc0;
+    shard_range(p, 0, &rb0, &rc0);
+    bool equal = true;
+    for (int r = 0; r < c->nranks; ++r) {
+        int64_t rb, rc;
+        shard_range(p, r, &rb, &rc);
+        equal = equal && rc == rc0 && rb == r * rc0;
+    }
+    ncclResult_t r = ncclSuccess;
+    if (equal) {
+        r = ncclAllGather(W + static_cast<size_t>(c->rank) * rc0 * N, W, static_cast<size_t>(rc0 * N),
+                          ncclFloat32, c->nccl, s);
+        return r == ncclSuccess ? TAG_OK : nccl_fail(r, "ncclAllGather(W shards)");
+    }
+    r = ncclGroupStart();
+    for (int q = 0; q < c->nranks && r == ncclSuccess; ++q) {
+        int64_t rb, rc;
+        shard_range(p, q, &rb, &rc);
+        if (rc == 0) continue;
+        r = ncclBroadcast(W + rb * N, W + rb * N, static_cast<size_t>(rc * N), ncclFloat32, q,
+                          c->nccl, s);
+    }
+    ncclResult_t e = ncclGroupEnd();
+    if (r != ncclSuccess) return nccl_fail(r, "ncclBroadcast(W shard)");
+    return e == ncclSuccess ? TAG_OK : nccl_fail(e, "ncclGroupEnd");
+}
+
+tag_status_t tag_sfb_sync_sharded_sgd(tag_sfb_plan_t p, const void* X, const void* dY, float* W,
+                                      float* v_shard, tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_sgd: NULL plan");
+    if (!p->d.fuse_sgd) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_sgd: plan has fuse_sgd = 0");
+    if (p->d.out_dtype != TAG_F32)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_sgd: needs out_dtype = F32");
+    int64_t rb, rc;
+    shard_range(p, p->comm->rank, &rb, &rc);
+    TAG_TRY(check_ptrs("tag_sfb_sync_sharded_sgd", {X, dY, W}));
+    if (rc > 0) TAG_TRY(check_ptrs("tag_sfb_sync_sharded_sgd", {v_shard}));
+    if (((rb * p->d.N * 4) & 15) != 0)
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_sgd: shard rows not 16-byte aligned");
+    TAG_TRY(set_device(p->comm));
+    TAG_TRY(check_async(p->comm));
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    float* Ws = W + rb * p->d.N;               // this rank's rows of W
+    void* none = nullptr;
+    if (fusable(p, nullptr, 1)) {
+        // one fused launch: push, reconstruct this rank's rows, SGD-momentum on them
+        TAG_TRY(fused_sync(&p, 1, &X, &dY, &none, true, &Ws, &v_shard, s, true));
+    } else {
+        TAG_TRY(do_gather(p, X, dY, s));
+        if (rc > 0) {
+            ReconArgs a{};
+            a.A = static_cast<const char*>(p->src_x) + rb * dtype_size(p->d.wire_dtype);
+            a.Bm = p->src_dy;
+            a.C = nullptr;
+            a.M = rc;
+            a.N = p->d.N;
+            a.K = p->K;
+            a.lda = p->d.M;
+            a.wire = p->d.wire_dtype;
+            a.out = p->d.out_dtype;
+            a.alpha = p->alpha;
+            a.sgd = true;
+            a.W = Ws;
+            a.V = v_shard;
+            a.lr = p->d.lr;
+            a.mu = p->d.momentum;
+            a.wd = p->d.weight_decay;
+            a.opt = 1;
+            TAG_TRY((p->use_tc && recon_tc_ok(a)) ? launch_recon_tc(a, s) : launch_recon_simt(a, s));
+        }
+    }
+    // parameter all-gather: every rank ends with the whole updated W (ZeRO-style)
+    return allgather_rows(p, W, s);
+}
+
 tag_status_t tag_sfb_sync_host(tag_sfb_plan_t p, const void* X_host, const void* dY_host,
                                void* dW_host, tag_stream_t stream) {
     if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_host: NULL plan");

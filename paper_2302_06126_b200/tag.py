@@ -106,6 +106,7 @@ _SIGS = {
     "tag_sfb_sync_host": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_shard_rows": ([_vp, _i, _p(ctypes.c_int64), _p(ctypes.c_int64)], _st),
     "tag_sfb_sync_sharded": ([_vp, _vp, _vp, _vp, _vp], _st),
+    "tag_sfb_sync_sharded_sgd": ([_vp, _vp, _vp, _vp, _vp, _vp], _st),
     "tag_local_grad": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_dense_allreduce": ([_vp, _vp, _vp], _st),
     "tag_ps_sync": ([_vp, _vp, _i, _vp], _st),
@@ -327,6 +328,16 @@ class SfbPlan:
         _check(_lib.tag_sfb_sync_sharded(self._h, x, dy, dw, _stream(stream)),
                "tag_sfb_sync_sharded")
         return dW_shard
+
+    def sync_sharded_sgd(self, X, dY, W, v_shard, stream=None):
+        """Sharded SGD-momentum on this rank's rows of W (momentum rows v_shard), then the W
+        all-gather: W (M x N fp32) is the whole updated parameter on every rank afterwards."""
+        x, dy = self._xy(X, dY)
+        _, rc = self.shard_rows()
+        v = self._dev(v_shard, torch.float32, (rc, self.N), "v_shard") if rc > 0 else _vp()
+        _check(_lib.tag_sfb_sync_sharded_sgd(self._h, x, dy,
+                                             self._dev(W, torch.float32, (self.M, self.N), "W"), v,
+                                             _stream(stream)), "tag_sfb_sync_sharded_sgd")
 
     def sync_host(self, X_host, dY_host, dW_host, stream=None):
         _check(_lib.tag_sfb_sync_host(

@@ -324,6 +324,29 @@ def main():
     record("ps_sync", okp, rel_fro=e)
     plan.close()
 
+    # 13: sharded SGD-momentum + W all-gather (f-2): W equals the replicated fused-SGD W bit for
+    #     bit on every rank, v_shard equals the same rows of the replicated v (equal shards ->
+    #     ncclAllGather; unequal / empty shards -> per-shard broadcasts)
+    oks = True
+    for li, (M, N, B) in enumerate([(4096, 1024, 32), (520, 264, 24), (96, 264, 32)]):
+        X, dY = synth.factors(66, li, rank, M, N, B, "normal", "small")
+        W0, v0 = synth.sgd_state(66, li, M, N)
+        plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", fuse_sgd=True, lr=1e-3,
+                           momentum=0.9, weight_decay=1e-4, gather=gather)
+        Xd, dYd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(dY).to(torch.bfloat16).cuda()
+        Wr, vr = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
+        rb, rc = plan.shard_rows()
+        Ws = Wr.clone()
+        vs = vr[rb:rb + rc].clone() if rc > 0 else torch.empty(1, N, device="cuda")[:0]
+        for _ in range(3):
+            plan.sync_sgd(Xd, dYd, Wr, vr, None)
+            plan.sync_sharded_sgd(Xd, dYd, Ws, vs)
+        torch.cuda.synchronize()
+        hashes = tdist.all_gather_object(digest(Ws))
+        oks = oks and torch.equal(Ws, Wr) and torch.equal(vs, vr[rb:rb + rc]) and len(set(hashes)) == 1
+        plan.close()
+    record("sharded_sgd_allgather", oks)
+
     # 7: selector identical on all ranks and equal to the oracle
     lays = [dict(M=L.M, N=L.N, B=L.B) for c in (2, 3, 4, 5) for L in synth.CONFIGS[c].layers]
     got = tag.select([dict(l, factor_dtype="bf16", grad_dtype="f32") for l in lays], n,

@@ -329,3 +329,22 @@ def test_multi_gpu_check_loopback(gather):
     assert res["ok"] and res["n"] == 1, res
     want = "nccl_allgather" if gather == "nccl" else "nvlink_push"
     assert want in res["gather_modes"], res
+
+
+def test_sharded_sgd_with_parameter_allgather(tag, loop):
+    """f-2 on one rank: the sharded SGD step (one shard = every row) through the fused exchange
+    equals the replicated fused SGD bit for bit, three steps (n = 2 / 4 with real shards:
+    scripts/multi_gpu_check.py, check 13)."""
+    M, N, B = 520, 264, 24
+    X, dY = synth.factors(66, 1, 0, M, N, B, "normal", "small")
+    W0, v0 = synth.sgd_state(66, 1, M, N)
+    plan = tag.SfbPlan(loop, M, N, B, fuse_sgd=True, lr=1e-3, momentum=0.9, weight_decay=1e-4)
+    Xd, dYd = dev(X, "bf16"), dev(dY, "bf16")
+    Wr, vr = torch.from_numpy(W0).cuda(), torch.from_numpy(v0).cuda()
+    Ws, vs = Wr.clone(), vr.clone()
+    for _ in range(3):
+        plan.sync_sgd(Xd, dYd, Wr, vr, None)
+        plan.sync_sharded_sgd(Xd, dYd, Ws, vs)
+    torch.cuda.synchronize()
+    assert torch.equal(Ws, Wr) and torch.equal(vs, vr)
+    plan.close()
