@@ -26,14 +26,20 @@ if a.group:
     for li, L in enumerate(cfg.layers):
         X, dY = synth.all_factors(cfg.cid, li, a.n, L.M, L.N, L.B, L.x_dist, L.dy_dist)
         K = a.n * L.B
-        plans.append(tag.SfbPlan(comm, L.M, L.N, K, "bf16", "bf16", a.out))
+        plans.append(tag.SfbPlan(comm, L.M, L.N, K, "bf16", "bf16", a.out, fuse_sgd=a.sgd, lr=1e-3,
+                                 momentum=0.9))
         Xs.append(torch.from_numpy(X.reshape(K, L.M)).to(torch.bfloat16).cuda())
         dYs.append(torch.from_numpy(dY.reshape(K, L.N)).to(torch.bfloat16).cuda())
         dWs.append(torch.empty(L.M, L.N, dtype=torch.float32 if a.out == "f32" else torch.bfloat16,
                                device="cuda"))
     g = tag.SfbGroup(plans)
+    Ws = [torch.zeros(p.M, p.N, device="cuda") for p in plans] if a.sgd else None
+    vs = [torch.zeros(p.M, p.N, device="cuda") for p in plans] if a.sgd else None
     for _ in range(a.iters):
-        g.sync(Xs, dYs, dWs)
+        if a.sgd:       # E2: the bench's --config 5 step (no dW stored)
+            g.sync_sgd(Xs, dYs, Ws, vs, None)
+        else:
+            g.sync(Xs, dYs, dWs)
     torch.cuda.synchronize()
     print(f"ok group config {a.config} n={a.n} iters={a.iters}")
     g.close()
