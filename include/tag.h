@@ -280,7 +280,7 @@ tag_status_t tag_sfb_bias_grad(tag_sfb_plan_t plan, void* db_out, tag_stream_t s
 /* ------------------------------------------------------------------------------------------ */
 /* Buckets: several layers synchronised together                                             */
 /* ------------------------------------------------------------------------------------------ */
-/* A group (bucket) of 1..8 plans of the same comm, the same in/wire/out dtypes and the same
+/* A group (bucket) of 1..32 plans of the same comm, the same in/wire/out dtypes and the same
  * fuse_sgd setting (and SGD hyper-parameters). tag_sfb_group_sync runs steps a1-a4 of every layer with ONE push kernel (one LSA
  * barrier; or one grouped NCCL call) and ONE persistent tensor-core launch over all layers' output
  * tiles, so launch latency, pipeline ramp-up, the last partial wave and the barrier latency are

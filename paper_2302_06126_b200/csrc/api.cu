@@ -339,11 +339,11 @@ tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int
         // plan's staging), then the unfused Adam kernel — the same arithmetic (optim.cuh)
         float* dw = static_cast<float*>(dW);
         if (!dw) {
-            if (!p->adam_dw) {
-                cudaError_t e = cudaMalloc(&p->adam_dw, static_cast<size_t>(p->d.M * p->d.N) * 4);
+            if (!p->adam_dw) {       // first use, stream-ordered
+                cudaError_t e = cudaMallocAsync(&p->adam_dw, static_cast<size_t>(p->d.M * p->d.N) * 4, s);
                 if (e != cudaSuccess) {
                     p->adam_dw = nullptr;
-                    return cuda_fail(e, "reconstruct: cudaMalloc(Adam staging)");
+                    return cuda_fail(e, "reconstruct: cudaMallocAsync(Adam staging)");
                 }
             }
             dw = p->adam_dw;
@@ -945,19 +945,20 @@ tag_status_t tag_sfb_sync_host(tag_sfb_plan_t p, const void* X_host, const void*
     const size_t bx = static_cast<size_t>(d.B * d.M) * dtype_size(d.in_dtype);
     const size_t bdy = static_cast<size_t>(d.B * d.N) * dtype_size(d.in_dtype);
     const size_t bdw = static_cast<size_t>(d.M * d.N) * dtype_size(d.out_dtype);
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (!p->st_x) {
-        cudaError_t e = cudaMalloc(&p->st_x, bx);
-        if (e == cudaSuccess) e = cudaMalloc(&p->st_dy, bdy);
-        if (e == cudaSuccess) e = cudaMalloc(&p->st_dw, bdw);
+        // device staging on first use, stream-ordered (no device-wide synchronisation)
+        cudaError_t e = cudaMallocAsync(&p->st_x, bx, s);
+        if (e == cudaSuccess) e = cudaMallocAsync(&p->st_dy, bdy, s);
+        if (e == cudaSuccess) e = cudaMallocAsync(&p->st_dw, bdw, s);
         if (e != cudaSuccess) {
-            cudaFree(p->st_x);
-            cudaFree(p->st_dy);
-            cudaFree(p->st_dw);
+            if (p->st_x) cudaFreeAsync(p->st_x, s);
+            if (p->st_dy) cudaFreeAsync(p->st_dy, s);
+            if (p->st_dw) cudaFreeAsync(p->st_dw, s);
             p->st_x = p->st_dy = p->st_dw = nullptr;
-            return cuda_fail(e, "tag_sfb_sync_host: cudaMalloc(staging)");
+            return cuda_fail(e, "tag_sfb_sync_host: cudaMallocAsync(staging)");
         }
     }
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMemcpyAsync(p->st_x, X_host, bx, cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(p->st_dy, dY_host, bdy, cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) return cuda_fail(e, "tag_sfb_sync_host: H2D copy");
@@ -1048,7 +1049,7 @@ tag_status_t tag_sgd_step(tag_sfb_plan_t p, const float* dW, float* W, float* v,
 tag_status_t tag_sfb_group_create(const tag_sfb_plan_t* plans, int count, tag_sfb_group_t* out) {
     if (!plans || !out) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_create: NULL argument");
     if (count < 1 || count > MAX_GROUP)
-        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_create: count must be in [1, 8]");
+        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_create: count must be in [1, 32]");
     for (int i = 0; i < count; ++i) {
         const tag_plan_s* p = plans[i];
         if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_create: NULL plan");

@@ -180,8 +180,14 @@ struct TileRef {
 // m0 is the first row of the (BM * CTAS)-row tile; CTA rank r of a pair owns rows m0 + r * BM.
 template <int BN, int CTAS>
 __device__ __forceinline__ TileRef locate(const GroupParams& gp, int tile) {
-    int li = 0;
-    while (li + 1 < gp.count && tile >= gp.L[li + 1].tile_begin) ++li;
+    // the last layer whose first tile is <= tile (binary search; empty shards share tile_begin
+    // with the next layer and are skipped)
+    int li = 0, hi = gp.count - 1;
+    while (li < hi) {
+        const int mid = (li + hi + 1) >> 1;
+        if (tile >= gp.L[mid].tile_begin) li = mid;
+        else hi = mid - 1;
+    }
     const int t = tile - gp.L[li].tile_begin;
     if (gp.L[li].m_fast) {
         const int nmb = gp.L[li].num_m_blocks;

@@ -79,7 +79,7 @@ struct FusedGather {
 bool recon_tc_ok(const ReconArgs& a);
 tag_status_t launch_recon_tc(const ReconArgs& a, cudaStream_t s);
 // Grouped form: one persistent launch over all layers' tiles (1 <= count <= MAX_GROUP).
-constexpr int MAX_GROUP = 8;
+constexpr int MAX_GROUP = 32;   // layers per bucket (kernel parameter space: ~15 KB at 32)
 // fused != nullptr: the kernel also pushes this rank's factors to every peer and waits per layer
 // on the arrival counters (see recon_tc.cu). recon_tc_grid: the CTA count such a launch uses.
 tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s,

@@ -348,3 +348,25 @@ def test_sharded_sgd_with_parameter_allgather(tag, loop):
     torch.cuda.synchronize()
     assert torch.equal(Ws, Wr) and torch.equal(vs, vr)
     plan.close()
+
+
+def test_fused_bucket_of_32_layers(tag, loop, oracle_mod):
+    """The fused exchange with the 32-layer bucket limit (32 per-layer arrival counters, one push
+    kernel) == the oracle, bit for bit, two calls (both window parities)."""
+    layers = [(256 + 64 * (i % 4), 264 + 8 * (i % 3), 24) for i in range(32)]
+    plans, Xs, dYs, wants = [], [], [], []
+    for li, (M, N, B) in enumerate(layers):
+        X, dY = ints(80 + li, M, N, B)
+        plans.append(tag.SfbPlan(loop, M, N, B))
+        Xs.append(dev(X, "bf16"))
+        dYs.append(dev(dY, "bf16"))
+        wants.append(want_int(oracle_mod, X, dY))
+    g = tag.SfbGroup(plans)
+    for _ in range(2):
+        outs = [torch.full((p.M, p.N), float("nan"), device="cuda") for p in plans]
+        g.sync(Xs, dYs, outs)
+        torch.cuda.synchronize()
+        assert all(same_bits(o, w) for o, w in zip(outs, wants))
+    g.close()
+    for p in plans:
+        p.close()

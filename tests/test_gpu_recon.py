@@ -361,6 +361,39 @@ def test_group_equals_per_plan(tag, comm1, layers, out_dt):
         p.close()
 
 
+def test_group_of_32_layers(tag, comm1):
+    """A whole 12-block FFN stack (24 layers, 768 x 3072 / 3072 x 768) plus 8 small layers — the
+    32-layer bucket limit — in one launch == per-layer syncs, bit for bit; 33 plans rejected."""
+    layers = [(768, 3072, 64) if i % 2 == 0 else (3072, 768, 64) for i in range(24)]
+    layers += [(136 + 8 * i, 264, 64) for i in range(8)]
+    plans, Xs, dYs, ref, got = [], [], [], [], []
+    for li, (M, N, K) in enumerate(layers):
+        X = synth.draw("int3", K, M, synth.rng(71, li, 0, 0))
+        dY = synth.draw("int3", K, N, synth.rng(71, li, 0, 1))
+        plan = tag.SfbPlan(comm1, M, N, K, "bf16", "bf16", "bf16")
+        plans.append(plan)
+        Xs.append(to_dev(X, "bf16"))
+        dYs.append(to_dev(dY, "bf16"))
+        r = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        plan.sync(Xs[-1], dYs[-1], r)
+        ref.append(r)
+        got.append(torch.full((M, N), float("nan"), dtype=torch.bfloat16, device="cuda"))
+    group = tag.SfbGroup(plans)
+    before = tag.kernel_launches()
+    group.sync(Xs, dYs, got)
+    torch.cuda.synchronize()
+    assert tag.kernel_launches() - before == 1
+    assert all(torch.equal(r, g) for r, g in zip(ref, got))
+    extra = tag.SfbPlan(comm1, 64, 32, 8, "bf16", "bf16", "bf16")
+    with pytest.raises(tag.TagError) as e:
+        tag.SfbGroup(plans + [extra])
+    assert e.value.status == tag.ERR_INVALID_ARG
+    extra.close()
+    group.close()
+    for p in plans:
+        p.close()
+
+
 def test_group_validation(tag, comm1):
     a = tag.SfbPlan(comm1, 64, 32, 8, "bf16", "bf16", "f32")
     b = tag.SfbPlan(comm1, 64, 32, 8, "bf16", "bf16", "bf16")
