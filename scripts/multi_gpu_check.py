@@ -347,6 +347,24 @@ def main():
         plan.close()
     record("sharded_sgd_allgather", oks)
 
+    # 14: full-size layers through the bench's launch configuration at this n — VGG-19 fc6
+    #     (25088 x 4096, B = 32; fused push, K = 32n) and the Transformer output projection
+    #     (512 x 32000, 256 tokens; K = 256n, column-sweep raster) — 4000 entries per layer against
+    #     the oracle computed one by one on the exact bf16 operands, rel. Frobenius <= 1e-5, and
+    #     dW bitwise identical on every rank
+    okf, errs = True, {}
+    for cid, li, M, N, B, xd, dyd in [(2, 0, 25088, 4096, 32, "relu", "masked_small"),
+                                      (4, 0, 512, 32000, 256, "normal", "softmax_onehot")]:
+        dW, dense, hashes, Xall, dYall, Xe, dYe = run(cid, li, M, N, B, xd, dyd, "bf16", "bf16", "f32")
+        idx = np.random.default_rng(11).integers(0, M * N, 4000)
+        ref = oracle.sfb_sum_entries(Xe, dYe, idx) / (n * B)
+        got = dW.cpu().numpy().ravel()[idx]
+        e = rel_fro(got, ref)
+        errs[f"{M}x{N}"] = e
+        okf = okf and e <= 1e-5 and len(set(hashes)) == 1 and np.isfinite(dW.cpu().numpy()).all()
+        del dW, dense
+    record("full_size_sampled", okf, rel_fro=errs)
+
     # 7: selector identical on all ranks and equal to the oracle
     lays = [dict(M=L.M, N=L.N, B=L.B) for c in (2, 3, 4, 5) for L in synth.CONFIGS[c].layers]
     got = tag.select([dict(l, factor_dtype="bf16", grad_dtype="f32") for l in lays], n,
