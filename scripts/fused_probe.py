@@ -18,10 +18,11 @@ from paper_2302_06126_b200 import synth, tag  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--label", default="product")
 ap.add_argument("--gather", default="auto")
+ap.add_argument("--multicast", action="store_true")
 args = ap.parse_args()
 rank, local_rank, world = tdist.init_from_env()
 torch.cuda.set_device(local_rank)
-comm = tdist.bootstrap_comm(tag, local_rank)
+comm = tdist.bootstrap_comm(tag, local_rank, multicast=args.multicast)
 cfg = synth.CONFIGS[2]
 plans, Xs, dYs, dWs = [], [], [], []
 for li, L in enumerate(cfg.layers):
@@ -53,6 +54,7 @@ t = tdist.max_over_ranks(statistics.median(ts))
 p10 = tdist.max_over_ranks(sorted(ts)[len(ts) // 10])
 if rank == 0:
     print(json.dumps({"n": world, "variant": args.label, "gather": args.gather,
+                      "multicast": args.multicast,
                       "lib": os.environ.get("TAG_LIB_PATH", "libtag.so"),
                       "step_us": round(t * 1e3, 2),
                       "p10_us": round(p10 * 1e3, 2)}),
