@@ -365,6 +365,59 @@ def main():
         del dW, dense
     record("full_size_sampled", okf, rel_fro=errs)
 
+    # 15: protocol stress — one set of plans driven by a seeded random mix of calls that share
+    #     their windows, parities and arrival counters (single syncs, bucket syncs with the plans in
+    #     different groups, staged gather + reconstruct, sharded syncs), integer inputs, every
+    #     result bit exact; the same sequence on every rank (collective order)
+    specs = [(520, 264, 24), (4096, 1000, 32), (256, 512, 32)]
+    plans, Xs, dYs, wants = [], [], [], []
+    for li, (M, N, B) in enumerate(specs):
+        X, dY = synth.factors(67, li, rank, M, N, B, "int3", "int3")
+        plans.append(tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", gather=gather))
+        Xs.append(torch.from_numpy(X).to(torch.bfloat16).cuda())
+        dYs.append(torch.from_numpy(dY).to(torch.bfloat16).cuda())
+        Xa, dYa = synth.all_factors(67, li, n, M, N, B, "int3", "int3")
+        wants.append(oracle.sfb_sum(Xa, dYa).astype(np.float32) * np.float32(1.0 / (n * B)))
+    g_all = tag.SfbGroup(plans)
+    g_pair = tag.SfbGroup([plans[2], plans[0]])
+    rs = np.random.default_rng(5)                # same seed on every rank: same call sequence
+    okst = True
+    for it in range(40):
+        op = int(rs.integers(0, 5))
+        outs = [torch.full((p.M, p.N), float("nan"), device="cuda") for p in plans]
+        if op == 0:
+            i = int(rs.integers(0, 3))
+            plans[i].sync(Xs[i], dYs[i], outs[i])
+            idx = [i]
+        elif op == 1:
+            g_all.sync(Xs, dYs, outs)
+            idx = [0, 1, 2]
+        elif op == 2:
+            g_pair.sync([Xs[2], Xs[0]], [dYs[2], dYs[0]], [outs[2], outs[0]])
+            idx = [2, 0]
+        elif op == 3:
+            i = int(rs.integers(0, 3))
+            plans[i].gather(Xs[i], dYs[i])
+            plans[i].reconstruct(outs[i])
+            idx = [i]
+        else:
+            i = int(rs.integers(0, 3))
+            rb, rc = plans[i].shard_rows()
+            sh = outs[i][rb:rb + rc] if rc > 0 else torch.empty(1, plans[i].N, device="cuda")[:0]
+            plans[i].sync_sharded(Xs[i], dYs[i], sh)
+            torch.cuda.synchronize()
+            okst = okst and (rc == 0 or np.array_equal(sh.cpu().numpy().view(np.uint32),
+                                                       wants[i][rb:rb + rc].view(np.uint32)))
+            continue
+        torch.cuda.synchronize()
+        for i in idx:
+            okst = okst and np.array_equal(outs[i].cpu().numpy().view(np.uint32), wants[i].view(np.uint32))
+    record("protocol_stress", okst)
+    g_pair.close()
+    g_all.close()
+    for p in plans:
+        p.close()
+
     # 7: selector identical on all ranks and equal to the oracle
     lays = [dict(M=L.M, N=L.N, B=L.B) for c in (2, 3, 4, 5) for L in synth.CONFIGS[c].layers]
     got = tag.select([dict(l, factor_dtype="bf16", grad_dtype="f32") for l in lays], n,
