@@ -22,6 +22,10 @@
  *   - dtype of X / dY = desc.in_dtype; of dW_out = desc.out_dtype. W and v are always fp32.
  *   - Every call that takes a cudaStream_t is stream-ordered and asynchronous: it only enqueues
  *     work; inputs must stay unmodified and all buffers alive until the stream passes the call.
+ *   - CUDA graphs: on a one-rank comm without NCCL the sync calls carry no per-call host state and
+ *     may be captured and replayed. Calls that exchange factors (n > 1, or a loopback comm) keep
+ *     per-call state on the host (which half of the double-buffered window, the arrival-counter
+ *     targets) and must not be captured.
  *   - Ownership: the caller owns X, dY, dW_out, W, v and all host buffers. The plan owns its
  *     gather buffers, staging buffers, TMA descriptors and NCCL reduction op; the comm owns the
  *     NCCL communicator. Destroy plans before their comm.

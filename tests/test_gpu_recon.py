@@ -670,3 +670,38 @@ def test_adam_validation(tag, comm1):
     with pytest.raises(tag.TagError):
         p.sync_sgd(X, dY, W, v)                             # not an SGD plan
     p.close()
+
+
+def test_cuda_graph_capture_n1(tag, comm1, oracle_mod):
+    """On a one-rank comm without NCCL a bucket sync is one kernel with no per-call host state, so
+    it can be captured in a CUDA graph and replayed (new inputs copied into the captured buffers
+    between replays); every replay is bit exact."""
+    layers = [(520, 264, 24), (4096, 1000, 32)]
+    plans = [tag.SfbPlan(comm1, M, N, K, "bf16", "bf16", "f32") for (M, N, K) in layers]
+    g = tag.SfbGroup(plans)
+    Xs = [torch.empty(K, M, dtype=torch.bfloat16, device="cuda") for (M, N, K) in layers]
+    dYs = [torch.empty(K, N, dtype=torch.bfloat16, device="cuda") for (M, N, K) in layers]
+    outs = [torch.empty(M, N, device="cuda") for (M, N, K) in layers]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g.sync(Xs, dYs, outs, s)                 # warm-up outside capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        g.sync(Xs, dYs, outs, s)
+    for rep in range(3):
+        wants = []
+        for li, (M, N, K) in enumerate(layers):
+            X = synth.draw("int3", K, M, synth.rng(90 + rep, li, 0, 0))
+            dY = synth.draw("int3", K, N, synth.rng(90 + rep, li, 0, 1))
+            Xs[li].copy_(torch.from_numpy(X).to(torch.bfloat16))
+            dYs[li].copy_(torch.from_numpy(dY).to(torch.bfloat16))
+            wants.append(expected_int(oracle_mod, X, dY, K, "f32"))
+        graph.replay()
+        torch.cuda.synchronize()
+        for o, w in zip(outs, wants):
+            assert np.array_equal(o.cpu().numpy().view(np.uint32), w.view(np.uint32))
+    g.close()
+    for p in plans:
+        p.close()
