@@ -22,10 +22,13 @@
  *   - dtype of X / dY = desc.in_dtype; of dW_out = desc.out_dtype. W and v are always fp32.
  *   - Every call that takes a cudaStream_t is stream-ordered and asynchronous: it only enqueues
  *     work; inputs must stay unmodified and all buffers alive until the stream passes the call.
- *   - CUDA graphs: on a one-rank comm without NCCL the sync calls carry no per-call host state and
- *     may be captured and replayed. Calls that exchange factors (n > 1, or a loopback comm) keep
- *     per-call state on the host (which half of the double-buffered window, the arrival-counter
- *     targets) and must not be captured.
+ *   - CUDA graphs: the calls keep no per-call state on the host. Which half of a plan's
+ *     double-buffered symmetric window a gather fills, and the arrival-counter targets of the fused
+ *     exchange, derive on the device from a call counter in the window, so tag_sfb_sync*, the group
+ *     calls, tag_sfb_gather / tag_sfb_reconstruct and the bias calls can be captured in a CUDA
+ *     graph and replayed (collectively: every rank replays the same sequence). Calls that go
+ *     through NCCL collectives (desc.gather = NCCL, tag_dense_allreduce, tag_ps_sync, the sharded
+ *     W all-gather) follow NCCL's own capture rules.
  *   - Ownership: the caller owns X, dY, dW_out, W, v and all host buffers. The plan owns its
  *     gather buffers, staging buffers, TMA descriptors and NCCL reduction op; the comm owns the
  *     NCCL communicator. Destroy plans before their comm.

@@ -100,14 +100,15 @@ struct tag_plan_s {
     void* win_base = nullptr;
     ncclWindow_t win = nullptr;
     size_t win_buf_bytes = 0;      // one buffer = K*(M+N)*e_w
-    size_t win_flag_off = 0;       // two u32 arrival counters (one per buffer parity)
-    uint32_t flag_total[2] = {0, 0};   // counter value after every fused call so far, per parity
-    uint32_t local_total[2] = {0, 0};  // local (hierarchical publish) counter, per parity
-    int parity = 0;
+    size_t win_flag_off = 0;       // the window flag area (WIN_* offsets, tag_internal.h)
+    uint32_t* flags = nullptr;     // the same area, this rank's device address
     void* lx = nullptr;            // local cast scratch for tag_local_grad (B x M, B x N wire)
     void* ldy = nullptr;
-    const void* src_x = nullptr;   // operands of the next reconstruct (set by gather)
-    const void* src_dy = nullptr;
+    const void* src_x = nullptr;   // operands of the next reconstruct (set by gather); for the
+    const void* src_dy = nullptr;  // window: buffer 0, with buffer 1 and the call counter below
+    const void* src_x1 = nullptr;  // (the buffer of the latest gather is read on the device)
+    const void* src_dy1 = nullptr;
+    const uint32_t* src_ctr = nullptr;
     ncclRedOp_t premul{};
     bool has_premul = false;
     // device staging of tag_sfb_sync_host (allocated on first use)
@@ -202,6 +203,46 @@ bool needs_gather_buffers(const tag_comm_s* c, const tag_sfb_desc_t& d) {
     return has_collective(c) || d.in_dtype != d.wire_dtype;
 }
 
+// The reconstruction operands of a plan: a plain buffer pair, or the symmetric window's two
+// buffers with its call counter (which buffer the latest gather filled is device state).
+void set_src_plain(tag_plan_s* p, const void* x, const void* dy) {
+    p->src_x = x;
+    p->src_dy = dy;
+    p->src_x1 = p->src_dy1 = nullptr;
+    p->src_ctr = nullptr;
+}
+
+size_t win_off_dy(const tag_plan_s* p) {
+    return static_cast<size_t>(p->K * p->d.M) * dtype_size(p->d.wire_dtype);
+}
+
+void set_src_window(tag_plan_s* p) {
+    char* w = static_cast<char*>(p->win_base);
+    p->src_x = w;
+    p->src_dy = w + win_off_dy(p);
+    p->src_x1 = w + p->win_buf_bytes;
+    p->src_dy1 = w + p->win_buf_bytes + win_off_dy(p);
+    p->src_ctr = p->flags + WIN_CALLS / 4;
+}
+
+// a's operands from the plan's latest gather; columns col0.. of X_all (sharded rows of dW)
+void fill_src(const tag_plan_s* p, ReconArgs& a, int64_t col0 = 0) {
+    const size_t xo = static_cast<size_t>(col0) * dtype_size(p->d.wire_dtype);
+    a.A = static_cast<const char*>(p->src_x) + xo;
+    a.Bm = p->src_dy;
+    if (p->src_ctr) {
+        a.A1 = static_cast<const char*>(p->src_x1) + xo;
+        a.Bm1 = p->src_dy1;
+        a.ctr = p->src_ctr;
+        a.ctr_mode = 1;
+    }
+}
+
+PushSegment push_segment(const tag_plan_s* p, const void* X, const void* dY) {
+    return PushSegment{X, dY, p->win, 0, win_off_dy(p), p->win_buf_bytes, p->win_flag_off, p->flags,
+                       p->d.B * p->d.M, p->d.B * p->d.N};
+}
+
 // Every rank's device work up to here is complete and every rank has reached this point: the
 // window of a new plan is zeroed everywhere before any peer can push into it (a late memset
 // would wipe a peer's factors and arrival counters), and on destroy no peer still writes into
@@ -224,26 +265,21 @@ tag_status_t do_gather(tag_plan_s* p, const void* X, const void* dY, cudaStream_
     const size_t ew = dtype_size(d.wire_dtype);
     if (!has_collective(p->comm)) {
         if (d.in_dtype == d.wire_dtype) {
-            p->src_x = X;
-            p->src_dy = dY;
+            set_src_plain(p, X, dY);
             return TAG_OK;
         }
         TAG_TRY(launch_pack(X, p->gx, cx, dY, p->gdy, cy, d.in_dtype, d.wire_dtype, s));
-        p->src_x = p->gx;
-        p->src_dy = p->gdy;
+        set_src_plain(p, p->gx, p->gdy);
         return TAG_OK;
     }
     const int r = p->comm->rank;
     if (p->gather_mode == TAG_GATHER_NVLINK_PUSH) {
-        // a1 + a2 fused: cast and store straight into every peer's window (push_gather.cu)
-        const size_t off_x = static_cast<size_t>(p->parity) * p->win_buf_bytes;
-        const size_t off_dy = off_x + static_cast<size_t>(p->K * d.M) * ew;
-        PushSegment seg{X, dY, p->win, off_x, off_dy, cx, cy};
+        // a1 + a2 fused: cast and store straight into every peer's window (push_gather.cu); the
+        // kernel picks the buffer from the window's call counter and advances it
+        PushSegment seg = push_segment(p, X, dY);
         TAG_TRY(launch_push_gather_group(p->comm->devcomm, &seg, 1, r, d.in_dtype, d.wire_dtype,
-                                         PUSH_MAX_CTAS, s));
-        p->src_x = static_cast<char*>(p->win_base) + off_x;
-        p->src_dy = static_cast<char*>(p->win_base) + off_dy;
-        p->parity ^= 1;
+                                         PUSH_MAX_CTAS, p->flags + WIN_LOCAL_PUSH / 4, s));
+        set_src_window(p);
         return TAG_OK;
     }
     char* gx = static_cast<char*>(p->gx);
@@ -266,8 +302,7 @@ tag_status_t do_gather(tag_plan_s* p, const void* X, const void* dY, cudaStream_
     ncclResult_t ne = ncclGroupEnd();
     if (nr != ncclSuccess) return nccl_fail(nr, "ncclAllGather");
     if (ne != ncclSuccess) return nccl_fail(ne, "ncclGroupEnd");
-    p->src_x = p->gx;
-    p->src_dy = p->gdy;
+    set_src_plain(p, p->gx, p->gdy);
     return TAG_OK;
 }
 
@@ -305,8 +340,7 @@ tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int
                       const AdamCall* adam = nullptr) {
     if (!p->src_x) return fail(TAG_ERR_INVALID_ARG, "reconstruct: no factors gathered on this plan yet");
     ReconArgs a{};
-    a.A = p->src_x;
-    a.Bm = p->src_dy;
+    fill_src(p, a);
     a.C = dW;
     a.M = p->d.M;
     a.N = p->d.N;
@@ -327,10 +361,15 @@ tag_status_t do_recon(tag_plan_s* p, void* dW, bool sgd, float* W, float* V, int
         const int64_t kp = (K + TF32_KALIGN - 1) / TF32_KALIGN * TF32_KALIGN;
         float* sx = static_cast<float*>(p->split);
         float* sdy = sx + 2 * kp * p->d.M;
-        TAG_TRY(launch_tf32_split(static_cast<const float*>(p->src_x), sx, K, p->d.M, kp, s));
-        TAG_TRY(launch_tf32_split(static_cast<const float*>(p->src_dy), sdy, K, p->d.N, kp, s));
+        TAG_TRY(launch_tf32_split(static_cast<const float*>(a.A), static_cast<const float*>(a.A1),
+                                  a.ctr, sx, K, p->d.M, kp, s));
+        TAG_TRY(launch_tf32_split(static_cast<const float*>(a.Bm), static_cast<const float*>(a.Bm1),
+                                  a.ctr, sdy, K, p->d.N, kp, s));
         a.A = sx;
         a.Bm = sdy;
+        a.A1 = a.Bm1 = nullptr;
+        a.ctr = nullptr;
+        a.ctr_mode = 0;
         a.kpad = kp;
     }
     if (p->use_tc && recon_tc_ok(a)) return launch_recon_tc(a, s);
@@ -411,11 +450,16 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
     for (int i = 0; i < count; ++i) {
         tag_plan_s* p = plans[i];
         const size_t ew = dtype_size(p->d.wire_dtype);
-        const size_t off_x = static_cast<size_t>(p->parity) * p->win_buf_bytes;
-        const size_t off_dy = off_x + static_cast<size_t>(p->K * p->d.M) * ew;
+        // both buffers of the window: the kernel pushes into, waits on and reads buffer c & 1 of
+        // the window's call counter c, and advances c (no per-call host state)
+        char* w = static_cast<char*>(p->win_base);
         a[i] = ReconArgs{};
-        a[i].A = static_cast<char*>(p->win_base) + off_x;
-        a[i].Bm = static_cast<char*>(p->win_base) + off_dy;
+        a[i].A = w;
+        a[i].Bm = w + win_off_dy(p);
+        a[i].A1 = w + p->win_buf_bytes;
+        a[i].Bm1 = w + p->win_buf_bytes + win_off_dy(p);
+        a[i].ctr = p->flags + WIN_CALLS / 4;
+        a[i].ctr_mode = 2;
         a[i].C = dW[i];
         a[i].M = p->d.M;
         a[i].N = p->d.N;
@@ -433,40 +477,30 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
         a[i].srcX = X[i];
         a[i].srcY = dY[i];
         a[i].win = p->win;
-        a[i].off_x = off_x;
-        a[i].off_dy = off_dy;
-        a[i].off_flag = p->win_flag_off + 4 * static_cast<size_t>(p->parity);
+        a[i].off_x = 0;
+        a[i].off_dy = win_off_dy(p);
+        a[i].buf_bytes = p->win_buf_bytes;
+        a[i].off_flag = p->win_flag_off;
+        a[i].flags = p->flags;
         a[i].cx = p->d.B * p->d.M;
         a[i].cy = p->d.B * p->d.N;
         if (sharded) {
             int64_t rb, rc;
             shard_range(p, c->rank, &rb, &rc);
-            a[i].A = static_cast<const char*>(a[i].A) + rb * ew;   // columns rb.. of X_all
+            a[i].A = static_cast<const char*>(a[i].A) + rb * ew;     // columns rb.. of X_all
+            a[i].A1 = static_cast<const char*>(a[i].A1) + rb * ew;
             a[i].lda = p->d.M;
             a[i].M = rc;
         }
     }
-    // hierarchical publish: the last CTA of every rank adds 1 per layer on every peer, so each
-    // arrival counter grows by exactly n per call whatever grid each rank launched (the local
-    // counter, which this rank's CTAs alone increment, tracks this rank's own grid)
-    const uint32_t grid = static_cast<uint32_t>(recon_tc_grid(a, count));
-    const uint32_t inc = static_cast<uint32_t>(c->nranks);
-    for (int i = 0; i < count; ++i) a[i].flag_target = plans[i]->flag_total[plans[i]->parity] + inc;
-    tag_plan_s* p0 = plans[0];
+    // hierarchical publish: the last CTA of every rank (plan 0's self-resetting local counter)
+    // adds 1 per layer on every peer, so each arrival counter grows by exactly n per call
+    // whatever grid each rank launched
     FusedGather fg{c->nranks, c->rank, c->mc_base,
                    plans[0]->d.in_dtype == TAG_F32 && plans[0]->d.wire_dtype == TAG_BF16,
-                   reinterpret_cast<uint32_t*>(static_cast<char*>(p0->win_base) +
-                                               p0->win_flag_off + 8 + 4 * p0->parity),
-                   p0->local_total[p0->parity] + grid};
-    p0->local_total[p0->parity] += grid;
+                   plans[0]->flags + WIN_LOCAL_FUSED / 4};
     TAG_TRY(launch_recon_tc_group(a, count, s, &fg));
-    for (int i = 0; i < count; ++i) {
-        tag_plan_s* p = plans[i];
-        p->flag_total[p->parity] += inc;
-        p->src_x = static_cast<char*>(p->win_base) + a[i].off_x;     // the full X_all
-        p->src_dy = a[i].Bm;
-        p->parity ^= 1;
-    }
+    for (int i = 0; i < count; ++i) set_src_window(plans[i]);
     return TAG_OK;
 }
 
@@ -634,7 +668,9 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
             cleanup();
             return nccl_fail(r, "tag_sfb_plan: symmetric gather window");
         }
-        // deterministic initial contents (every slot is overwritten by its owner before use)
+        p->flags = reinterpret_cast<uint32_t*>(static_cast<char*>(p->win_base) + p->win_flag_off);
+        // deterministic initial contents (every slot is overwritten by its owner before use); the
+        // call counter and the arrival / local counters start at 0
         cudaError_t e = cudaMemset(p->win_base, 0, bytes);
         if (e != cudaSuccess) {
             cleanup();
@@ -807,7 +843,8 @@ tag_status_t tag_sfb_bias_grad(tag_sfb_plan_t p, void* db_out, tag_stream_t stre
     if (!p || !db_out) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_bias_grad: NULL argument");
     if (!p->src_dy) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_bias_grad: no factors gathered on this plan yet");
     TAG_TRY(set_device(p->comm));
-    BiasArgs a{p->src_dy, db_out, p->K, p->d.N, p->d.wire_dtype, p->d.out_dtype, p->alpha};
+    BiasArgs a{p->src_dy, p->src_dy1, p->src_ctr, db_out, p->K, p->d.N, p->d.wire_dtype,
+               p->d.out_dtype, p->alpha};
     return launch_bias_grad(&a, 1, reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -834,12 +871,8 @@ tag_status_t tag_sfb_sync_sharded(tag_sfb_plan_t p, const void* X, const void* d
         return fused_sync(&p, 1, &X, &dY, &dW_shard, false, nullptr, nullptr, s, true);
     TAG_TRY(do_gather(p, X, dY, s));
     if (rc == 0) return TAG_OK;
-    const size_t ew = dtype_size(p->d.wire_dtype);
-    const void* full_x = p->src_x;
-    p->src_x = static_cast<const char*>(full_x) + rb * ew;
     ReconArgs a{};
-    a.A = p->src_x;
-    a.Bm = p->src_dy;
+    fill_src(p, a, rb);
     a.C = dW_shard;
     a.M = rc;
     a.N = p->d.N;
@@ -848,9 +881,7 @@ tag_status_t tag_sfb_sync_sharded(tag_sfb_plan_t p, const void* X, const void* d
     a.wire = p->d.wire_dtype;
     a.out = p->d.out_dtype;
     a.alpha = p->alpha;
-    tag_status_t st = (p->use_tc && recon_tc_ok(a)) ? launch_recon_tc(a, s) : launch_recon_simt(a, s);
-    p->src_x = full_x;
-    return st;
+    return (p->use_tc && recon_tc_ok(a)) ? launch_recon_tc(a, s) : launch_recon_simt(a, s);
 }
 
 // Parameter all-gather of the sharded optimizer step: rank r's rows [rb_r, rb_r + rc_r) of W
@@ -911,8 +942,7 @@ tag_status_t tag_sfb_sync_sharded_sgd(tag_sfb_plan_t p, const void* X, const voi
         TAG_TRY(do_gather(p, X, dY, s));
         if (rc > 0) {
             ReconArgs a{};
-            a.A = static_cast<const char*>(p->src_x) + rb * dtype_size(p->d.wire_dtype);
-            a.Bm = p->src_dy;
+            fill_src(p, a, rb);
             a.C = nullptr;
             a.M = rc;
             a.N = p->d.N;
@@ -983,14 +1013,12 @@ tag_status_t tag_local_grad(tag_sfb_plan_t p, const void* X, const void* dY, voi
         void* lx = p->lx ? p->lx : static_cast<char*>(p->gx) + r * d.B * d.M * ew;
         void* ldy = p->ldy ? p->ldy : static_cast<char*>(p->gdy) + r * d.B * d.N * ew;
         TAG_TRY(launch_pack(X, lx, d.B * d.M, dY, ldy, d.B * d.N, d.in_dtype, d.wire_dtype, s));
-        p->src_x = lx;
-        p->src_dy = ldy;
+        set_src_plain(p, lx, ldy);
     } else {
-        p->src_x = X;
-        p->src_dy = dY;
+        set_src_plain(p, X, dY);
     }
     tag_status_t st = do_recon(p, dW_local, false, nullptr, nullptr, d.B, 1.0f, s);
-    p->src_x = p->src_dy = nullptr;   // a later reconstruct needs a fresh gather
+    set_src_plain(p, nullptr, nullptr);   // a later reconstruct needs a fresh gather
     return st;
 }
 
@@ -1099,22 +1127,11 @@ tag_status_t tag_sfb_group_gather(tag_sfb_group_t g, const void* const* X, const
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if (g->push_all) {
         PushSegment seg[MAX_GROUP];
-        for (int i = 0; i < count; ++i) {
-            tag_plan_s* p = g->plans[i];
-            const size_t ew = dtype_size(p->d.wire_dtype);
-            const size_t off_x = static_cast<size_t>(p->parity) * p->win_buf_bytes;
-            const size_t off_dy = off_x + static_cast<size_t>(p->K * p->d.M) * ew;
-            seg[i] = PushSegment{X[i], dY[i], p->win, off_x, off_dy, p->d.B * p->d.M, p->d.B * p->d.N};
-        }
+        for (int i = 0; i < count; ++i) seg[i] = push_segment(g->plans[i], X[i], dY[i]);
         tag_plan_s* p0 = g->plans[0];
         TAG_TRY(launch_push_gather_group(c->devcomm, seg, count, c->rank, p0->d.in_dtype,
-                                         p0->d.wire_dtype, PUSH_MAX_CTAS, s));
-        for (int i = 0; i < count; ++i) {
-            tag_plan_s* p = g->plans[i];
-            p->src_x = static_cast<char*>(p->win_base) + seg[i].off_x;
-            p->src_dy = static_cast<char*>(p->win_base) + seg[i].off_dy;
-            p->parity ^= 1;
-        }
+                                         p0->d.wire_dtype, PUSH_MAX_CTAS, p0->flags + WIN_LOCAL_PUSH / 4, s));
+        for (int i = 0; i < count; ++i) set_src_window(g->plans[i]);
         return TAG_OK;
     }
     // mixed / NCCL mode: one NCCL group around every plan's gather (nested groups are legal)
@@ -1149,8 +1166,7 @@ static tag_status_t group_reconstruct(tag_sfb_group_t g, void* const* dW, bool s
     for (int i = 0; i < count; ++i) {
         tag_plan_s* p = g->plans[i];
         a[i] = ReconArgs{};
-        a[i].A = p->src_x;
-        a[i].Bm = p->src_dy;
+        fill_src(p, a[i]);
         a[i].C = dW[i];
         a[i].M = p->d.M;
         a[i].N = p->d.N;
@@ -1190,7 +1206,8 @@ tag_status_t tag_sfb_group_bias_grad(tag_sfb_group_t g, void* const* db, tag_str
         if (!db[i]) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_bias_grad: NULL db entry");
         if (!p->src_dy)
             return fail(TAG_ERR_INVALID_ARG, "tag_sfb_group_bias_grad: no factors gathered yet");
-        a[i] = BiasArgs{p->src_dy, db[i], p->K, p->d.N, p->d.wire_dtype, p->d.out_dtype, p->alpha};
+        a[i] = BiasArgs{p->src_dy, p->src_dy1, p->src_ctr, db[i], p->K, p->d.N, p->d.wire_dtype,
+                        p->d.out_dtype, p->alpha};
     }
     TAG_TRY(set_device(g->plans[0]->comm));
     return launch_bias_grad(a, count, reinterpret_cast<cudaStream_t>(stream));
@@ -1275,8 +1292,7 @@ tag_status_t tag_sfb_group_sync_sharded(tag_sfb_group_t g, const void* const* X,
         shard_range(p, p->comm->rank, &rb, &rc);
         if (rc == 0) continue;
         ReconArgs r{};
-        r.A = static_cast<const char*>(p->src_x) + rb * dtype_size(p->d.wire_dtype);
-        r.Bm = p->src_dy;
+        fill_src(p, r, rb);
         r.C = dW[i];
         r.M = rc;
         r.N = p->d.N;

@@ -35,7 +35,8 @@ __device__ __forceinline__ float ld_f(const T* p) {
 
 template <typename T>
 __device__ __forceinline__ void accumulate(const BiasArgs& a, int64_t col0, int phase, float (&acc)[8]) {
-    const T* dy = static_cast<const T*>(a.dy);
+    // a window source: the buffer of the latest gather (device state, see tag_internal.h)
+    const T* dy = static_cast<const T*>(((load_calls(a.ctr) - 1u) & 1u) ? a.dy1 : a.dy);
     const bool vec = sizeof(T) == 2 && a.N % 8 == 0 && col0 + 8 <= a.N;
     for (int64_t k = phase; k < a.K; k += PHASES) {
         const T* row = dy + k * a.N + col0;

@@ -154,8 +154,11 @@ namespace {
 // 3xTF32 split (recon_tc.cu X3): one element per thread-iteration, grid-stride; non-finite
 // values keep hi = value (truncated) and lo = 0 (no inf - inf).
 __global__ void __launch_bounds__(256)
-tf32_split_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_t K, int64_t cols,
+tf32_split_kernel(const float* __restrict__ src0, const float* __restrict__ src1,
+                  const uint32_t* ctr, float* __restrict__ dst, int64_t K, int64_t cols,
                   int64_t kpad) {
+    // a window source: the buffer of the latest gather (device state, see tag_internal.h)
+    const float* src = ((load_calls(ctr) - 1u) & 1u) ? src1 : src0;
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t total = kpad * cols;
@@ -184,10 +187,10 @@ tf32_split_kernel(const float* __restrict__ src, float* __restrict__ dst, int64_
 }
 }  // namespace
 
-tag_status_t launch_tf32_split(const float* src, float* dst, int64_t K, int64_t cols, int64_t kpad,
-                               cudaStream_t s) {
+tag_status_t launch_tf32_split(const float* src, const float* src1, const uint32_t* ctr, float* dst,
+                               int64_t K, int64_t cols, int64_t kpad, cudaStream_t s) {
     if (kpad * cols == 0) return TAG_OK;
-    tf32_split_kernel<<<grid_for(kpad * cols), 256, 0, s>>>(src, dst, K, cols, kpad);
+    tf32_split_kernel<<<grid_for(kpad * cols), 256, 0, s>>>(src, src1, ctr, dst, K, cols, kpad);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "launch tf32_split_kernel");
     count_launch();

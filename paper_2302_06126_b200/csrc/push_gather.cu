@@ -42,7 +42,10 @@ struct PushLayer {
     const void* X;
     const void* dY;
     ncclWindow_t win;
-    size_t off_x, off_dy;   // byte offsets of X_all / dY_all of the current buffer in `win`
+    size_t off_x, off_dy;   // byte offsets of buffer 0's X_all / dY_all in `win`
+    size_t buf_bytes;       // buffer 1 = buffer 0 + buf_bytes
+    size_t off_flag;        // the window flag area (WIN_* offsets)
+    uint32_t* flags;        // the same area, this rank's address
     int64_t vx, vy;         // 16-byte output vectors of this rank's X_r / dY_r
     int64_t vbegin;         // first global vector index of this layer
 };
@@ -52,6 +55,7 @@ struct PushGroup {
     int count;
     int64_t total;
     int slot;               // this rank's slot (world rank)
+    uint32_t* local_ctr;    // self-resetting "last CTA" counter (plan 0's WIN_LOCAL_PUSH)
 };
 
 // DBG (diagnostics builds only: scripts/build_variant.sh -DEXP_PUSH_DBG=k, never the product):
@@ -75,6 +79,10 @@ push_gather_kernel(const ncclDevComm comm, const __grid_constant__ PushGroup g)
     const int me = comm.lsaRank;
     const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t nthreads = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    // this gather's buffer of every layer: c & 1 (device state, see tag_internal.h)
+    __shared__ uint32_t s_calls[MAX_GROUP];
+    if (threadIdx.x < g.count) s_calls[threadIdx.x] = load_calls(g.L[threadIdx.x].flags + WIN_CALLS / 4);
+    __syncthreads();
     int li = 0;
     for (int64_t v = tid; v < (DBG == 1 ? 0 : g.total); v += nthreads) {
         while (li + 1 < g.count && v >= g.L[li + 1].vbegin) ++li;   // v only grows
@@ -92,8 +100,9 @@ push_gather_kernel(const ncclDevComm comm, const __grid_constant__ PushGroup g)
         } else {
             val = __ldcs(reinterpret_cast<const uint4*>(isx ? L.X : L.dY) + i);
         }
-        const size_t off = isx ? L.off_x + (static_cast<size_t>(g.slot) * L.vx + i) * 16
-                               : L.off_dy + (static_cast<size_t>(g.slot) * L.vy + i) * 16;
+        const size_t pb = (s_calls[li] & 1u) * L.buf_bytes;
+        const size_t off = isx ? L.off_x + pb + (static_cast<size_t>(g.slot) * L.vx + i) * 16
+                               : L.off_dy + pb + (static_cast<size_t>(g.slot) * L.vy + i) * 16;
         for (int k = 0; k < npeers; ++k) {
             const int p = (me + k) % npeers;   // rotate so the senders spread over receivers
             *reinterpret_cast<uint4*>(ncclGetLsaPointer(L.win, off, p)) = val;
@@ -108,6 +117,26 @@ push_gather_kernel(const ncclDevComm comm, const __grid_constant__ PushGroup g)
     if constexpr (DBG != 2) {
         ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), comm, ncclTeamTagLsa(), blockIdx.x);
         bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+    }
+    // The last CTA of this rank (self-resetting counter: every CTA has read c by then) keeps the
+    // window's device state in step with the fused path: one arrival per layer on every peer
+    // (fused calls wait for n arrivals per call and buffer) and c advanced by one.
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t old;
+        asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;"
+                     : "=r"(old) : "l"(g.local_ctr), "r"(gridDim.x - 1) : "memory");
+        if (old == gridDim.x - 1) {
+            for (int l = 0; l < g.count; ++l) {
+                const size_t fo = g.L[l].off_flag + WIN_ARRIVAL + 4 * (s_calls[l] & 1u);
+                for (int k = 0; k < npeers; ++k) {
+                    const int p = (me + k) % npeers;
+                    uint32_t* ctr = static_cast<uint32_t*>(ncclGetLsaPointer(g.L[l].win, fo, p));
+                    asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" :: "l"(ctr) : "memory");
+                }
+                atomicAdd(g.L[l].flags + WIN_CALLS / 4, 1u);
+            }
+        }
     }
     if constexpr (DBG == 3) {
         if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1 || blockIdx.x == gridDim.x / 2))
@@ -177,7 +206,7 @@ int push_grid(int64_t vectors, int max_ctas) {
 
 tag_status_t launch_push_gather_group(const void* dc, const PushSegment* seg, int count, int slot,
                                       tag_dtype_t in, tag_dtype_t wire, int max_ctas,
-                                      cudaStream_t s) {
+                                      uint32_t* local_ctr, cudaStream_t s) {
     if (count < 1 || count > MAX_GROUP) return fail(TAG_ERR_INVALID_ARG, "push group size");
     const ncclDevComm& comm = *static_cast<const ncclDevComm*>(dc);
     const int64_t ew = static_cast<int64_t>(dtype_size(wire));
@@ -191,6 +220,9 @@ tag_status_t launch_push_gather_group(const void* dc, const PushSegment* seg, in
         L.win = static_cast<ncclWindow_t>(seg[i].win);
         L.off_x = seg[i].off_x;
         L.off_dy = seg[i].off_dy;
+        L.buf_bytes = seg[i].buf_bytes;
+        L.off_flag = seg[i].off_flag;
+        L.flags = seg[i].flags;
         L.vx = seg[i].cx * ew / 16;
         L.vy = seg[i].cy * ew / 16;
         L.vbegin = total;
@@ -199,6 +231,7 @@ tag_status_t launch_push_gather_group(const void* dc, const PushSegment* seg, in
     g.count = count;
     g.total = total;
     g.slot = slot;
+    g.local_ctr = local_ctr;
     const int grid = push_grid(total, max_ctas);
     if (in == wire)
         push_gather_kernel<false, EXP_PUSH_DBG><<<grid, PUSH_THREADS, 0, s>>>(comm, g);

@@ -23,10 +23,15 @@ __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return _
 
 template <typename T, bool OUT_BF16, bool SGD>
 __global__ void __launch_bounds__(256)
-recon_simt_kernel(const T* __restrict__ A, const T* __restrict__ Bm, void* __restrict__ C,
+recon_simt_kernel(const T* __restrict__ A0, const T* __restrict__ B0, const T* __restrict__ A1,
+                  const T* __restrict__ B1, const uint32_t* ctr, void* __restrict__ C,
                   int M, int N, int K, int64_t lda, float alpha, float* __restrict__ W,
                   float* __restrict__ V, float lr, float mu, float wd)
 {
+    // window operands: the buffer of the latest gather (device state, see tag_internal.h)
+    const bool one = (load_calls(ctr) - 1u) & 1u;
+    const T* __restrict__ A = one ? A1 : A0;
+    const T* __restrict__ Bm = one ? B1 : B0;
     __shared__ float As[TK][TM];
     __shared__ float Bs[TK][TN];
     const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
@@ -84,7 +89,8 @@ tag_status_t launch_t(const ReconArgs& a, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>((a.N + TN - 1) / TN), static_cast<unsigned>((a.M + TM - 1) / TM));
     if (grid.y > 65535) return fail(TAG_ERR_UNSUPPORTED, "recon_simt: M too large");
     recon_simt_kernel<T, OUT_BF16, SGD><<<grid, 256, 0, s>>>(
-        static_cast<const T*>(a.A), static_cast<const T*>(a.Bm), a.C, static_cast<int>(a.M),
+        static_cast<const T*>(a.A), static_cast<const T*>(a.Bm), static_cast<const T*>(a.A1),
+        static_cast<const T*>(a.Bm1), a.ctr_mode == 1 ? a.ctr : nullptr, a.C, static_cast<int>(a.M),
         static_cast<int>(a.N), static_cast<int>(a.K), a.lda ? a.lda : a.M, a.alpha, a.W, a.V, a.lr,
         a.mu, a.wd);
     cudaError_t e = cudaGetLastError();

@@ -138,6 +138,9 @@ struct Cfg {
 struct LayerParams {
     CUtensorMap tmA;  // X_all (K x M) bf16, box 64 x BK, 128-B swizzle (X3: [hi;lo] fp32, box 32 x BK)
     CUtensorMap tmB;  // dY_all (K x N)
+    CUtensorMap tmA1, tmB1;   // window operands: the same maps on buffer 1 (ctr_mode != 0)
+    const uint32_t* ctr;      // window operands: the window's call counter (WIN_CALLS), else null
+    int ctr_mode;             // 0: tmA / tmB; 1: buffer (c - 1) & 1 (latest gather); 2: c & 1 (FUSED)
     void* C;          // dW out (may be nullptr with SGD)
     float* W;
     float* V;         // SGD momentum buffer / Adam second moment
@@ -154,9 +157,11 @@ struct LayerParams {
     const void* srcX;      // X_r (B x M, wire dtype)
     const void* srcY;      // dY_r (B x N)
     ncclWindow_t win;      // the layer's symmetric window
-    uint64_t off_x, off_dy, off_flag;   // this call's X_all / dY_all buffer and arrival counter
+    uint64_t off_x, off_dy;  // buffer 0's X_all / dY_all in the window (buffer 1: + buf_bytes)
+    uint64_t buf_bytes;
+    uint64_t off_flag;     // the window flag area (WIN_* offsets)
+    uint32_t* flags;       // the same area, this rank's address
     int64_t vx, vy;        // 16-byte vectors of X_r / dY_r
-    uint32_t flag_target;  // arrival count that means "every rank's factors have landed"
 };
 
 struct GroupParams {
@@ -169,8 +174,7 @@ struct GroupParams {
     int slot;              // this rank (its slot in X_all / dY_all)
     char* mc_base;         // FUSED: NVLS multicast base of the windows, or nullptr (unicast)
     int cast;              // FUSED: the sources are fp32, cast to bf16 (RNE) on the way out
-    uint32_t* local_ctr;   // FUSED: hierarchical publish counter (FusedGather::local_ctr)
-    uint32_t local_target;
+    uint32_t* local_ctr;   // FUSED: self-resetting hierarchical publish counter
 };
 
 struct TileRef {
@@ -236,7 +240,8 @@ __device__ unsigned long long g_dbg_stamps[160 * DBG_SLOTS];
 #define DBG_STAMP(slot) ((void)0)
 #endif
 
-__device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, int me) {
+__device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, int me,
+                                           uint32_t (&calls)[MAX_GROUP]) {
     if (threadIdx.x == 0) DBG_STAMP(0);
     const int64_t G = gridDim.x;
 #ifndef EXP_PUSH_U
@@ -247,6 +252,12 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
     for (int li = 0; li < gp.count; ++li) {
         const LayerParams& L = gp.L[li];
         const int64_t V = L.vx + L.vy;
+        // this call's buffer: c & 1 of the window's call counter (device state); each thread
+        // loads c itself (before this CTA arrives on the local counter, hence before the last CTA
+        // advances c) so the load overlaps its first factor loads (no CTA barrier); the
+        // producer thread keeps the values for its arrival targets and buffer choice
+        calls[li] = load_calls(L.ctr);
+        const size_t pb = (calls[li] & 1u) * L.buf_bytes;
         const int64_t beg = V * blockIdx.x / G, end = V * (blockIdx.x + 1) / G;
         for (int64_t v0 = beg + threadIdx.x; v0 < end; v0 += U * static_cast<int64_t>(blockDim.x)) {
             uint4 val[U];
@@ -265,8 +276,8 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
                 } else {
                     val[u] = __ldcs(reinterpret_cast<const uint4*>(isx ? L.srcX : L.srcY) + i);
                 }
-                off[u] = isx ? L.off_x + (static_cast<size_t>(gp.slot) * L.vx + i) * 16
-                             : L.off_dy + (static_cast<size_t>(gp.slot) * L.vy + i) * 16;
+                off[u] = isx ? L.off_x + pb + (static_cast<size_t>(gp.slot) * L.vx + i) * 16
+                             : L.off_dy + pb + (static_cast<size_t>(gp.slot) * L.vy + i) * 16;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -297,26 +308,30 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
         asm volatile("fence.acq_rel.sys;" ::: "memory");
         DBG_STAMP(3);
         {
+            // self-resetting: the last of the gridDim.x CTAs reads gridDim.x - 1 and leaves 0
             uint32_t old;
-            asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;"
-                         : "=r"(old) : "l"(gp.local_ctr) : "memory");
+            asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;"
+                         : "=r"(old) : "l"(gp.local_ctr), "r"(gridDim.x - 1) : "memory");
             DBG_STAMP(4);
-            if (old + 1 != gp.local_target) return;        // not the last CTA of this rank
+            if (old != gridDim.x - 1) return;              // not the last CTA of this rank
             // every other CTA's slice was released at system scope before its local add,
             // which this acquire observed; make that cumulative for the peers
             asm volatile("fence.acq_rel.sys;" ::: "memory");
         }
         for (int li = 0; li < gp.count; ++li) {
+            const size_t fo = gp.L[li].off_flag + WIN_ARRIVAL + 4 * (calls[li] & 1u);
             if (mc != nullptr) {
                 asm volatile("multimem.red.relaxed.sys.global.add.u32 [%0], 1;"
-                             :: "l"(mc_ptr(mc, gp.L[li].win, gp.L[li].off_flag)) : "memory");
+                             :: "l"(mc_ptr(mc, gp.L[li].win, fo)) : "memory");
             } else {
                 for (int k = 0; k < npeers; ++k) {
                     const int p = (me + k) % npeers;
-                    uint32_t* ctr = static_cast<uint32_t*>(ncclGetLsaPointer(gp.L[li].win, gp.L[li].off_flag, p));
+                    uint32_t* ctr = static_cast<uint32_t*>(ncclGetLsaPointer(gp.L[li].win, fo, p));
                     asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" :: "l"(ctr) : "memory");
                 }
             }
+            // every CTA of this rank has read c (it arrived on the local counter after its push)
+            atomicAdd(gp.L[li].flags + WIN_CALLS / 4, 1u);
         }
         DBG_STAMP(5);
     }
@@ -324,13 +339,18 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
 
 // Producer side: wait until every rank's every CTA has published layer li (acquire, system
 // scope), then order those generic-proxy writes before the async-proxy (TMA) reads.
-__device__ __forceinline__ void fused_wait(const LayerParams& L, int me) {
-    const uint32_t* ctr = static_cast<const uint32_t*>(ncclGetLsaPointer(L.win, L.off_flag, me));
+__device__ __forceinline__ void fused_wait(const LayerParams& L, int me, int npeers, uint32_t calls) {
+    // every rank adds 1 per call to the counter of the call's buffer, and c is the same on every
+    // rank, so call c is complete everywhere when the counter of buffer c & 1 reaches
+    // n * (floor(c / 2) + 1)
+    const uint32_t target = static_cast<uint32_t>(npeers) * (calls / 2u + 1u);
+    const uint32_t* ctr = static_cast<const uint32_t*>(
+        ncclGetLsaPointer(L.win, L.off_flag + WIN_ARRIVAL + 4 * (calls & 1u), me));
     const uint64_t t0 = gtimer();
     while (true) {
         uint32_t got;
         asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(got) : "l"(ctr) : "memory");
-        if (static_cast<int32_t>(got - L.flag_target) >= 0) break;
+        if (static_cast<int32_t>(got - target) >= 0) break;
         if (gtimer() - t0 > 10ull * 1000 * 1000 * 1000) __trap();   // a peer never arrived (10 s)
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -371,6 +391,10 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
             if (gp.L[i].M == 0) continue;             // empty shard: no tensor maps
             ptx::tma_prefetch_desc(&gp.L[i].tmA);
             ptx::tma_prefetch_desc(&gp.L[i].tmB);
+            if (gp.L[i].ctr_mode) {
+                ptx::tma_prefetch_desc(&gp.L[i].tmA1);
+                ptx::tma_prefetch_desc(&gp.L[i].tmB1);
+            }
         }
         for (int s = 0; s < C::STAGES; ++s) {
             ptx::mbar_init(bar_full + 8 * s, CTAS);      // pair: the leader's, armed by both
@@ -395,8 +419,10 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
     grid_dep_wait();
     // Diagnostics builds only (scripts/build_variant.sh -DEXP_FUSED_DBG=k, never the product):
     // 1 = no push and no wait, 2 = push without the arrival wait, 3 = phase stamps.
+    uint32_t calls[MAX_GROUP];                // window operands: each layer's call counter c
     if constexpr (FUSED) {
-        if (EXP_FUSED_DBG != 1) fused_push(gp, npeers, me);
+        if (EXP_FUSED_DBG != 1) fused_push(gp, npeers, me, calls);
+        else for (int i = 0; i < gp.count; ++i) calls[i] = load_calls(gp.L[i].ctr);
     }
 
     if (warp == 0) {
@@ -404,18 +430,27 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            uint32_t ready = 0;               // FUSED: layers whose factors have all landed
+            uint32_t ready = 0;               // layers whose call counter (and, FUSED, factors) are known
             for (int tile = unit; tile < gp.num_tiles; tile += nunits) {
                 const TileRef tr = locate<BN, CTAS>(gp, tile);
-                if constexpr (FUSED) {
-                    if (!(ready & (1u << tr.li))) {
-                        if (EXP_FUSED_DBG == 0 || EXP_FUSED_DBG == 3) fused_wait(gp.L[tr.li], me);
+                const LayerParams& Lp = gp.L[tr.li];
+                if (!(ready & (1u << tr.li))) {
+                    // FUSED: c was read before this CTA's push (the kernel advances it later);
+                    // a reconstruction of an earlier gather reads it here
+                    if (!FUSED) calls[tr.li] = Lp.ctr_mode ? load_calls(Lp.ctr) : 1u;
+                    if constexpr (FUSED) {
+                        if (EXP_FUSED_DBG == 0 || EXP_FUSED_DBG == 3)
+                            fused_wait(Lp, me, npeers, calls[tr.li]);
                         if (ready == 0) DBG_STAMP(6);
-                        ready |= 1u << tr.li;
                     }
+                    ready |= 1u << tr.li;
                 }
-                const CUtensorMap* tmA = &gp.L[tr.li].tmA;
-                const CUtensorMap* tmB = &gp.L[tr.li].tmB;
+                // window operands: the FUSED kernel reads its own gather's buffer (c & 1), a
+                // later reconstruction the latest gather's ((c - 1) & 1)
+                const uint32_t cc = calls[tr.li];
+                const bool buf1 = Lp.ctr_mode == 2 ? (cc & 1u) : Lp.ctr_mode == 1 ? ((cc - 1u) & 1u) : false;
+                const CUtensorMap* tmA = buf1 ? &Lp.tmA1 : &Lp.tmA;
+                const CUtensorMap* tmB = buf1 ? &Lp.tmB1 : &Lp.tmB;
                 const int nkb = gp.L[tr.li].num_k_blocks;
                 for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait(bar_empty + 8 * stage, phase ^ 1);
@@ -980,14 +1015,25 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
         if (a[i].M == 0) {
             // an empty row shard (sharded sync, more ranks than 128-row tiles): no tiles and no
             // tensor maps; in a FUSED launch the layer's factors are still pushed to the peers
-        } else if (L.box3) {
-            if (!encode_3d(&L.tmA, a[i].A, orows, a[i].M, C::BK, C::A_CHUNKS, a[i].lda) ||
-                !encode_3d(&L.tmB, a[i].Bm, orows, a[i].N, C::BK, C::B_CHUNKS))
-                return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed for the factor operands");
-        } else if (!encode_2d(&L.tmA, a[i].A, odt, oes, orows, a[i].M, C::ELEMS, C::BK, a[i].lda, oswz) ||
-                   !encode_2d(&L.tmB, a[i].Bm, odt, oes, orows, a[i].N, C::ELEMS, C::BK, 0, oswz)) {
-            return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
+        } else {
+            // buffer 0 (or the only buffer), and for window operands buffer 1 as well
+            for (int buf = 0; buf < (a[i].ctr_mode ? 2 : 1); ++buf) {
+                CUtensorMap* mA = buf ? &L.tmA1 : &L.tmA;
+                CUtensorMap* mB = buf ? &L.tmB1 : &L.tmB;
+                const void* pA = buf ? a[i].A1 : a[i].A;
+                const void* pB = buf ? a[i].Bm1 : a[i].Bm;
+                if (L.box3) {
+                    if (!encode_3d(mA, pA, orows, a[i].M, C::BK, C::A_CHUNKS, a[i].lda) ||
+                        !encode_3d(mB, pB, orows, a[i].N, C::BK, C::B_CHUNKS))
+                        return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed for the factor operands");
+                } else if (!encode_2d(mA, pA, odt, oes, orows, a[i].M, C::ELEMS, C::BK, a[i].lda, oswz) ||
+                           !encode_2d(mB, pB, odt, oes, orows, a[i].N, C::ELEMS, C::BK, 0, oswz)) {
+                    return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
+                }
+            }
         }
+        L.ctr = a[i].ctr;
+        L.ctr_mode = a[i].ctr ? a[i].ctr_mode : 0;
         L.k_lo = X3 ? static_cast<int>(a[i].kpad) : 0;
         L.C = a[i].C;
         L.W = a[i].W;
@@ -1011,10 +1057,11 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
             L.win = static_cast<ncclWindow_t>(a[i].win);
             L.off_x = a[i].off_x;
             L.off_dy = a[i].off_dy;
+            L.buf_bytes = a[i].buf_bytes;
             L.off_flag = a[i].off_flag;
+            L.flags = a[i].flags;
             L.vx = a[i].cx * 2 / 16;
             L.vy = a[i].cy * 2 / 16;
-            L.flag_target = a[i].flag_target;
         }
     }
     gp.count = count;
@@ -1029,7 +1076,6 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     gp.mc_base = FUSED ? static_cast<char*>(fg->mc_base) : nullptr;
     gp.cast = FUSED && fg->cast ? 1 : 0;
     gp.local_ctr = FUSED ? fg->local_ctr : nullptr;
-    gp.local_target = FUSED ? fg->local_target : 0;
     auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED, X3, LONGK>;
     // the shared-memory opt-in, once per instantiation and device (thread-safe)
     static std::atomic<uint64_t> attr_set{0};
@@ -1151,12 +1197,6 @@ void recon_tc_describe(const ReconArgs* a, int count, int* bn, int* ctas, int* b
     *bn = wide ? 256 : 128;
     *ctas = wide ? use_ctas(a, count) : 1;
     *box3d = !EXP_RECON_NO3D && a[0].M % 64 == 0 && a[0].N % 64 == 0 && a[0].lda % 64 == 0 ? 1 : 0;
-}
-
-int recon_tc_grid(const ReconArgs* a, int count) {
-    const bool wide = big_tiles(a, count);
-    const int ctas = wide ? use_ctas(a, count) : 1;
-    return grid_for(tiles_for(a, count, wide ? 256 : 128, ctas), ctas, true);
 }
 
 tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s,

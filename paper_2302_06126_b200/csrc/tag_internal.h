@@ -35,9 +35,35 @@ inline size_t dtype_size(tag_dtype_t t) { return t == TAG_F32 ? 4 : 2; }
 // ------------------------------------------------------------------ reconstruction kernels
 // dW[m][j] = alpha * sum_{k<K} A[k][m] * Bm[k][j] (A: K x M, Bm: K x N, row-major, wire dtype),
 // written as out dtype (epilogue E1), or with the fused SGD-momentum update (epilogue E2).
+// The factors a plan gathered into its double-buffered symmetric window live in one of two
+// buffers; which one is device state: the window's call counter c (u32, WIN_CALLS below) counts
+// every kernel that gathered into the window, so the latest gather used buffer (c - 1) & 1 and a
+// gather in flight uses c & 1. Kernels read c on the device instead of taking the buffer from the
+// host, which keeps the sync calls free of per-call host state (CUDA-graph capturable).
+// Layout of each plan's window flag area (byte offsets from win_flag_off, all u32):
+constexpr int WIN_ARRIVAL = 0;      // [2] arrival counters, one per buffer (peers add to them)
+constexpr int WIN_LOCAL_FUSED = 8;  // self-resetting "last CTA" counter of the fused kernel
+constexpr int WIN_LOCAL_PUSH = 12;  // the same for the push-gather kernel
+constexpr int WIN_CALLS = 16;       // c
+
+// Read the call counter of a window (nullptr: a plain single buffer, parity 0). L1 is bypassed:
+// the value was written by an earlier kernel of the stream.
+__device__ __forceinline__ uint32_t load_calls(const uint32_t* ctr) {
+    if (ctr == nullptr) return 1u;   // (1 - 1) & 1 = buffer 0
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    return v;
+}
+
 struct ReconArgs {
     const void* A;       // K x M
     const void* Bm;      // K x N
+    // window operands: A / Bm are buffer 0, A1 / Bm1 buffer 1, ctr the window's call counter;
+    // ctr_mode 1: read the latest gather ((c - 1) & 1), 2: the fused kernel's own (c & 1)
+    const void* A1;
+    const void* Bm1;
+    const uint32_t* ctr;
+    int ctr_mode;
     void* C;             // M x N, out dtype; may be nullptr when sgd (no dW write)
     int64_t M, N, K;
     int64_t lda;         // elements between consecutive rows of A (0: M) — row shards of X_all
@@ -59,9 +85,11 @@ struct ReconArgs {
     const void* srcX;      // X_r, dY_r (in dtype: wire dtype, or fp32 with FusedGather::cast)
     const void* srcY;
     void* win;             // ncclWindow_t of the layer's symmetric window
-    uint64_t off_x, off_dy, off_flag;
+    uint64_t off_x, off_dy;  // buffer 0's X_all / dY_all in the window (buffer 1: + buf_bytes)
+    uint64_t buf_bytes;
+    uint64_t off_flag;     // the window flag area (WIN_* offsets)
+    uint32_t* flags;       // the same area, this rank's device address
     int64_t cx, cy;        // elements of X_r / dY_r
-    uint32_t flag_target;  // arrival-counter value meaning "all ranks' factors landed"
 };
 
 struct FusedGather {
@@ -69,10 +97,10 @@ struct FusedGather {
     int me;                // LSA rank (== comm rank)
     void* mc_base;         // NVLS multicast base (multimem.st to every GPU at once), or nullptr
     bool cast;             // sources are fp32, the wire is bf16 (RNE cast inside the push)
-    // hierarchical publish: CTAs count themselves on a local counter; the last one of this rank
-    // adds 1 to every layer's counter on every peer (n remote atomics per layer, not n * grid)
-    uint32_t* local_ctr;   // device address (this rank's window)
-    uint32_t local_target; // local counter value after this launch's CTAs have all arrived
+    // hierarchical publish: CTAs count themselves on a self-resetting local counter (plan 0's
+    // WIN_LOCAL_FUSED); the last one of this rank adds 1 to every layer's arrival counter on
+    // every peer (n remote atomics per layer, not n * grid) and advances every layer's c
+    uint32_t* local_ctr;
 };
 
 // Tensor-core path (tcgen05 + TMEM + TMA). Requires 16-byte aligned rows (see recon_tc_ok).
@@ -81,10 +109,9 @@ tag_status_t launch_recon_tc(const ReconArgs& a, cudaStream_t s);
 // Grouped form: one persistent launch over all layers' tiles (1 <= count <= MAX_GROUP).
 constexpr int MAX_GROUP = 32;   // layers per bucket (kernel parameter space: ~15 KB at 32)
 // fused != nullptr: the kernel also pushes this rank's factors to every peer and waits per layer
-// on the arrival counters (see recon_tc.cu). recon_tc_grid: the CTA count such a launch uses.
+// on the arrival counters (see recon_tc.cu).
 tag_status_t launch_recon_tc_group(const ReconArgs* a, int count, cudaStream_t s,
                                    const FusedGather* fused = nullptr);
-int recon_tc_grid(const ReconArgs* a, int count);
 // the tile configuration launch_recon_tc_group picks for these layers
 void recon_tc_describe(const ReconArgs* a, int count, int* bn, int* ctas, int* box3d);
 // SIMT FFMA path: any shape, fp32 or bf16 operands (exact fp32 accumulation in k order).
@@ -101,16 +128,22 @@ struct PushSegment {
     const void* X;
     const void* dY;
     void* win;              // ncclWindow_t
-    size_t off_x, off_dy;   // byte offsets of this buffer's X_all / dY_all in the window
+    size_t off_x, off_dy;   // byte offsets of buffer 0's X_all / dY_all in the window
+    size_t buf_bytes;       // buffer 1 = buffer 0 + buf_bytes
+    size_t off_flag;        // the window flag area (WIN_* offsets)
+    uint32_t* flags;        // the same area, this rank's device address
     int64_t cx, cy;         // elements of this rank's X_r / dY_r
 };
+// local_ctr: plan 0's WIN_LOCAL_PUSH (the last CTA after the barrier publishes and advances c)
 tag_status_t launch_push_gather_group(const void* dc, const PushSegment* seg, int count, int slot,
                                       tag_dtype_t in, tag_dtype_t wire, int max_ctas,
-                                      cudaStream_t s);
+                                      uint32_t* local_ctr, cudaStream_t s);
 
 // ------------------------------------------------------------------ bias gradient (R17)
 struct BiasArgs {
-    const void* dy;        // dY_all (K x N, wire dtype)
+    const void* dy;        // dY_all (K x N, wire dtype); a window: buffer 0
+    const void* dy1;       // window buffer 1, or nullptr
+    const uint32_t* ctr;   // the window's call counter (latest gather), or nullptr
     void* db;              // N, out dtype
     int64_t K, N;
     tag_dtype_t wire, out;
@@ -122,8 +155,8 @@ tag_status_t launch_bias_grad(const BiasArgs* a, int count, cudaStream_t s);
 // ------------------------------------------------------------------ 3xTF32 operand split
 // dst = [hi ; lo] (2*kpad x cols fp32): hi = src rounded to the nearest tf32 (a value kind::tf32
 // reads exactly), lo = src - hi (exact in fp32); rows [K, kpad) of both halves are zero.
-tag_status_t launch_tf32_split(const float* src, float* dst, int64_t K, int64_t cols, int64_t kpad,
-                               cudaStream_t s);
+tag_status_t launch_tf32_split(const float* src, const float* src1, const uint32_t* ctr, float* dst,
+                               int64_t K, int64_t cols, int64_t kpad, cudaStream_t s);
 constexpr int TF32_KALIGN = 16;   // kpad = K rounded up to the 3xTF32 stage depth
 
 // ------------------------------------------------------------------ unfused Adam (R22)

@@ -370,3 +370,51 @@ def test_fused_bucket_of_32_layers(tag, loop, oracle_mod):
     g.close()
     for p in plans:
         p.close()
+
+
+def test_cuda_graph_capture_exchange(tag, loop, oracle_mod):
+    """The window's buffer choice and arrival targets are device state (the window call counter),
+    so the fused exchange (a bucket sync), the staged push + reconstruct and the bias gradient can
+    be captured once and replayed, interleaved with ordinary calls; every replay is bit exact."""
+    layers = [(520, 264, 24), (4096, 1000, 32)]
+    plans = [tag.SfbPlan(loop, M, N, B) for (M, N, B) in layers]
+    g = tag.SfbGroup(plans)
+    Xs = [torch.empty(B, M, dtype=torch.bfloat16, device="cuda") for (M, N, B) in layers]
+    dYs = [torch.empty(B, N, dtype=torch.bfloat16, device="cuda") for (M, N, B) in layers]
+    outs = [torch.empty(M, N, device="cuda") for (M, N, B) in layers]
+    outs2 = [torch.empty(M, N, device="cuda") for (M, N, B) in layers]
+    dbs = [torch.empty(N, device="cuda") for (M, N, B) in layers]
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        g.sync(Xs, dYs, outs, s)                  # warm-up outside capture
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        g.sync(Xs, dYs, outs, s)                  # fused exchange + reconstruction
+        plans[1].gather(Xs[1], dYs[1], s)         # staged push + LSA barrier
+        plans[1].reconstruct(outs2[1], s)
+        for p, db in zip(plans, dbs):
+            p.bias_grad(db, s)
+    for rep in range(4):
+        wants, bwant = [], []
+        for li, (M, N, B) in enumerate(layers):
+            X, dY = ints(100 + rep * 7 + li, M, N, B)
+            Xs[li].copy_(torch.from_numpy(X).to(torch.bfloat16))
+            dYs[li].copy_(torch.from_numpy(dY).to(torch.bfloat16))
+            wants.append(want_int(oracle_mod, X, dY))
+            bwant.append(oracle_mod.sfb_bias_sum(dY[None]).astype(np.float32) * np.float32(1.0 / B))
+        graph.replay()
+        torch.cuda.synchronize()
+        assert all(same_bits(o, w) for o, w in zip(outs, wants))
+        assert same_bits(outs2[1], wants[1])
+        assert all(np.array_equal(d.cpu().numpy().view(np.uint32), w.view(np.uint32))
+                   for d, w in zip(dbs, bwant))
+        if rep % 2 == 0:                          # an ordinary call between replays
+            o = torch.full((layers[0][0], layers[0][1]), float("nan"), device="cuda")
+            plans[0].sync(Xs[0], dYs[0], o)
+            torch.cuda.synchronize()
+            assert same_bits(o, wants[0])
+    g.close()
+    for p in plans:
+        p.close()
