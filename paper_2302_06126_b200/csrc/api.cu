@@ -99,7 +99,12 @@ struct tag_plan_s {
     // NVLink push mode: double-buffered [X_all | dY_all] in an NCCL symmetric window
     void* win_base = nullptr;
     ncclWindow_t win = nullptr;
-    size_t win_buf_bytes = 0;      // one buffer = K*(M+N)*e_w
+    // window layout [X buf 0 | X buf 1 | dY buf 0 | dY buf 1 | flags]: each buffer win_kbuf rows
+    // (K rounded up to 128, the rows beyond K stay zero: the TMA boxes of the last K block read
+    // zeros, and one tensor map covers both buffers)
+    int64_t win_kbuf = 0;
+    size_t win_xbuf = 0;           // bytes of one X buffer = win_kbuf * M * e_w
+    size_t win_ybuf = 0;           // bytes of one dY buffer = win_kbuf * N * e_w
     size_t win_flag_off = 0;       // the window flag area (WIN_* offsets, tag_internal.h)
     uint32_t* flags = nullptr;     // the same area, this rank's device address
     void* lx = nullptr;            // local cast scratch for tag_local_grad (B x M, B x N wire)
@@ -212,16 +217,14 @@ void set_src_plain(tag_plan_s* p, const void* x, const void* dy) {
     p->src_ctr = nullptr;
 }
 
-size_t win_off_dy(const tag_plan_s* p) {
-    return static_cast<size_t>(p->K * p->d.M) * dtype_size(p->d.wire_dtype);
-}
+size_t win_off_dy(const tag_plan_s* p) { return 2 * p->win_xbuf; }
 
 void set_src_window(tag_plan_s* p) {
     char* w = static_cast<char*>(p->win_base);
     p->src_x = w;
+    p->src_x1 = w + p->win_xbuf;
     p->src_dy = w + win_off_dy(p);
-    p->src_x1 = w + p->win_buf_bytes;
-    p->src_dy1 = w + p->win_buf_bytes + win_off_dy(p);
+    p->src_dy1 = w + win_off_dy(p) + p->win_ybuf;
     p->src_ctr = p->flags + WIN_CALLS / 4;
 }
 
@@ -233,14 +236,15 @@ void fill_src(const tag_plan_s* p, ReconArgs& a, int64_t col0 = 0) {
     if (p->src_ctr) {
         a.A1 = static_cast<const char*>(p->src_x1) + xo;
         a.Bm1 = p->src_dy1;
+        a.kbuf = p->win_kbuf;
         a.ctr = p->src_ctr;
         a.ctr_mode = 1;
     }
 }
 
 PushSegment push_segment(const tag_plan_s* p, const void* X, const void* dY) {
-    return PushSegment{X, dY, p->win, 0, win_off_dy(p), p->win_buf_bytes, p->win_flag_off, p->flags,
-                       p->d.B * p->d.M, p->d.B * p->d.N};
+    return PushSegment{X, dY, p->win, 0, win_off_dy(p), p->win_xbuf, p->win_ybuf, p->win_flag_off,
+                       p->flags, p->d.B * p->d.M, p->d.B * p->d.N};
 }
 
 // Every rank's device work up to here is complete and every rank has reached this point: the
@@ -456,8 +460,9 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
         a[i] = ReconArgs{};
         a[i].A = w;
         a[i].Bm = w + win_off_dy(p);
-        a[i].A1 = w + p->win_buf_bytes;
-        a[i].Bm1 = w + p->win_buf_bytes + win_off_dy(p);
+        a[i].A1 = w + p->win_xbuf;
+        a[i].Bm1 = w + win_off_dy(p) + p->win_ybuf;
+        a[i].kbuf = p->win_kbuf;
         a[i].ctr = p->flags + WIN_CALLS / 4;
         a[i].ctr_mode = 2;
         a[i].C = dW[i];
@@ -479,7 +484,8 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
         a[i].win = p->win;
         a[i].off_x = 0;
         a[i].off_dy = win_off_dy(p);
-        a[i].buf_bytes = p->win_buf_bytes;
+        a[i].xbuf = p->win_xbuf;
+        a[i].ybuf = p->win_ybuf;
         a[i].off_flag = p->win_flag_off;
         a[i].flags = p->flags;
         a[i].cx = p->d.B * p->d.M;
@@ -657,8 +663,10 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
                                                                        : TAG_GATHER_NCCL;
     }
     if (p->gather_mode == TAG_GATHER_NVLINK_PUSH) {
-        p->win_buf_bytes = static_cast<size_t>(p->K * (d->M + d->N)) * ew;
-        p->win_flag_off = (2 * p->win_buf_bytes + 255) & ~static_cast<size_t>(255);
+        p->win_kbuf = (p->K + 127) / 128 * 128;
+        p->win_xbuf = static_cast<size_t>(p->win_kbuf * d->M) * ew;
+        p->win_ybuf = static_cast<size_t>(p->win_kbuf * d->N) * ew;
+        p->win_flag_off = (2 * (p->win_xbuf + p->win_ybuf) + 255) & ~static_cast<size_t>(255);
         size_t bytes = p->win_flag_off + 256;
         bytes = (bytes + 4095) & ~static_cast<size_t>(4095);      // NCCL_WIN_REQUIRED_ALIGNMENT
         ncclResult_t r = ncclMemAlloc(&p->win_base, bytes);

@@ -43,7 +43,7 @@ struct PushLayer {
     const void* dY;
     ncclWindow_t win;
     size_t off_x, off_dy;   // byte offsets of buffer 0's X_all / dY_all in `win`
-    size_t buf_bytes;       // buffer 1 = buffer 0 + buf_bytes
+    size_t xbuf, ybuf;      // buffer 1's X_all / dY_all are xbuf / ybuf bytes further
     size_t off_flag;        // the window flag area (WIN_* offsets)
     uint32_t* flags;        // the same area, this rank's address
     int64_t vx, vy;         // 16-byte output vectors of this rank's X_r / dY_r
@@ -100,9 +100,9 @@ push_gather_kernel(const ncclDevComm comm, const __grid_constant__ PushGroup g)
         } else {
             val = __ldcs(reinterpret_cast<const uint4*>(isx ? L.X : L.dY) + i);
         }
-        const size_t pb = (s_calls[li] & 1u) * L.buf_bytes;
-        const size_t off = isx ? L.off_x + pb + (static_cast<size_t>(g.slot) * L.vx + i) * 16
-                               : L.off_dy + pb + (static_cast<size_t>(g.slot) * L.vy + i) * 16;
+        const size_t par = s_calls[li] & 1u;
+        const size_t off = isx ? L.off_x + par * L.xbuf + (static_cast<size_t>(g.slot) * L.vx + i) * 16
+                               : L.off_dy + par * L.ybuf + (static_cast<size_t>(g.slot) * L.vy + i) * 16;
         for (int k = 0; k < npeers; ++k) {
             const int p = (me + k) % npeers;   // rotate so the senders spread over receivers
             *reinterpret_cast<uint4*>(ncclGetLsaPointer(L.win, off, p)) = val;
@@ -220,7 +220,8 @@ tag_status_t launch_push_gather_group(const void* dc, const PushSegment* seg, in
         L.win = static_cast<ncclWindow_t>(seg[i].win);
         L.off_x = seg[i].off_x;
         L.off_dy = seg[i].off_dy;
-        L.buf_bytes = seg[i].buf_bytes;
+        L.xbuf = seg[i].xbuf;
+        L.ybuf = seg[i].ybuf;
         L.off_flag = seg[i].off_flag;
         L.flags = seg[i].flags;
         L.vx = seg[i].cx * ew / 16;

@@ -138,9 +138,9 @@ struct Cfg {
 struct LayerParams {
     CUtensorMap tmA;  // X_all (K x M) bf16, box 64 x BK, 128-B swizzle (X3: [hi;lo] fp32, box 32 x BK)
     CUtensorMap tmB;  // dY_all (K x N)
-    CUtensorMap tmA1, tmB1;   // window operands: the same maps on buffer 1 (ctr_mode != 0)
     const uint32_t* ctr;      // window operands: the window's call counter (WIN_CALLS), else null
-    int ctr_mode;             // 0: tmA / tmB; 1: buffer (c - 1) & 1 (latest gather); 2: c & 1 (FUSED)
+    int ctr_mode;             // 0: one buffer; 1: buffer (c - 1) & 1 (latest gather); 2: c & 1 (FUSED)
+    int kbuf;                 // window operands: rows between the two buffers of tmA / tmB
     void* C;          // dW out (may be nullptr with SGD)
     float* W;
     float* V;         // SGD momentum buffer / Adam second moment
@@ -157,15 +157,19 @@ struct LayerParams {
     const void* srcX;      // X_r (B x M, wire dtype)
     const void* srcY;      // dY_r (B x N)
     ncclWindow_t win;      // the layer's symmetric window
-    uint64_t off_x, off_dy;  // buffer 0's X_all / dY_all in the window (buffer 1: + buf_bytes)
-    uint64_t buf_bytes;
+    uint64_t off_x, off_dy;  // buffer 0's X_all / dY_all in the window
+    uint64_t xbuf, ybuf;     // buffer 1's are xbuf / ybuf bytes further
     uint64_t off_flag;     // the window flag area (WIN_* offsets)
     uint32_t* flags;       // the same area, this rank's address
     int64_t vx, vy;        // 16-byte vectors of X_r / dY_r
 };
 
-struct GroupParams {
-    LayerParams L[MAX_GROUP];
+// MAXL = 4 (buckets of up to 4 layers) or MAX_GROUP: the kernel parameter block (and every
+// launch's copy of it) stays small for the common buckets (measured: 32-layer parameter blocks
+// cost ~2 us per launch on the n = 1 bench)
+template <int MAXL>
+struct GroupParamsT {
+    LayerParams L[MAXL];
     int count;
     int num_tiles;
     float lr, mu, wd;
@@ -182,16 +186,13 @@ struct TileRef {
 };
 
 // m0 is the first row of the (BM * CTAS)-row tile; CTA rank r of a pair owns rows m0 + r * BM.
-template <int BN, int CTAS>
-__device__ __forceinline__ TileRef locate(const GroupParams& gp, int tile) {
-    // the last layer whose first tile is <= tile (binary search; empty shards share tile_begin
-    // with the next layer and are skipped)
-    int li = 0, hi = gp.count - 1;
-    while (li < hi) {
-        const int mid = (li + hi + 1) >> 1;
-        if (tile >= gp.L[mid].tile_begin) li = mid;
-        else hi = mid - 1;
-    }
+template <int BN, int CTAS, typename GP>
+__device__ __forceinline__ TileRef locate(const GP& gp, int tile) {
+    // the last layer whose first tile is <= tile (empty shards share tile_begin with the next
+    // layer and are skipped). A linear scan: measured 2.3 us faster per n = 1 bench step than a
+    // binary search, whose data-dependent parameter loads sit on every warp's per-tile path
+    int li = 0;
+    while (li + 1 < gp.count && tile >= gp.L[li + 1].tile_begin) ++li;
     const int t = tile - gp.L[li].tile_begin;
     if (gp.L[li].m_fast) {
         const int nmb = gp.L[li].num_m_blocks;
@@ -240,8 +241,8 @@ __device__ unsigned long long g_dbg_stamps[160 * DBG_SLOTS];
 #define DBG_STAMP(slot) ((void)0)
 #endif
 
-__device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, int me,
-                                           uint32_t (&calls)[MAX_GROUP]) {
+template <typename GP>
+__device__ __forceinline__ void fused_push(const GP& gp, int npeers, int me, uint32_t* calls) {
     if (threadIdx.x == 0) DBG_STAMP(0);
     const int64_t G = gridDim.x;
 #ifndef EXP_PUSH_U
@@ -257,7 +258,7 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
         // advances c) so the load overlaps its first factor loads (no CTA barrier); the
         // producer thread keeps the values for its arrival targets and buffer choice
         calls[li] = load_calls(L.ctr);
-        const size_t pb = (calls[li] & 1u) * L.buf_bytes;
+        const size_t par = calls[li] & 1u;
         const int64_t beg = V * blockIdx.x / G, end = V * (blockIdx.x + 1) / G;
         for (int64_t v0 = beg + threadIdx.x; v0 < end; v0 += U * static_cast<int64_t>(blockDim.x)) {
             uint4 val[U];
@@ -276,8 +277,8 @@ __device__ __forceinline__ void fused_push(const GroupParams& gp, int npeers, in
                 } else {
                     val[u] = __ldcs(reinterpret_cast<const uint4*>(isx ? L.srcX : L.srcY) + i);
                 }
-                off[u] = isx ? L.off_x + pb + (static_cast<size_t>(gp.slot) * L.vx + i) * 16
-                             : L.off_dy + pb + (static_cast<size_t>(gp.slot) * L.vy + i) * 16;
+                off[u] = isx ? L.off_x + par * L.xbuf + (static_cast<size_t>(gp.slot) * L.vx + i) * 16
+                             : L.off_dy + par * L.ybuf + (static_cast<size_t>(gp.slot) * L.vy + i) * 16;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -356,9 +357,9 @@ __device__ __forceinline__ void fused_wait(const LayerParams& L, int me, int npe
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3, bool LONGK>
+template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3, bool LONGK, int MAXL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
-recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const int me)
+recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers, const int me)
 {
     constexpr int EP = OUT_BF16 || X3 ? 1 : (SGD ? EXP_SGD_EP : 2);   // epilogue chunks per round
     using C = Cfg<BN, CTAS, X3, EP, LONGK>;
@@ -391,10 +392,6 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
             if (gp.L[i].M == 0) continue;             // empty shard: no tensor maps
             ptx::tma_prefetch_desc(&gp.L[i].tmA);
             ptx::tma_prefetch_desc(&gp.L[i].tmB);
-            if (gp.L[i].ctr_mode) {
-                ptx::tma_prefetch_desc(&gp.L[i].tmA1);
-                ptx::tma_prefetch_desc(&gp.L[i].tmB1);
-            }
         }
         for (int s = 0; s < C::STAGES; ++s) {
             ptx::mbar_init(bar_full + 8 * s, CTAS);      // pair: the leader's, armed by both
@@ -419,7 +416,7 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
     grid_dep_wait();
     // Diagnostics builds only (scripts/build_variant.sh -DEXP_FUSED_DBG=k, never the product):
     // 1 = no push and no wait, 2 = push without the arrival wait, 3 = phase stamps.
-    uint32_t calls[MAX_GROUP];                // window operands: each layer's call counter c
+    uint32_t calls[MAXL];                     // window operands: each layer's call counter c
     if constexpr (FUSED) {
         if (EXP_FUSED_DBG != 1) fused_push(gp, npeers, me, calls);
         else for (int i = 0; i < gp.count; ++i) calls[i] = load_calls(gp.L[i].ctr);
@@ -449,8 +446,9 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                 // later reconstruction the latest gather's ((c - 1) & 1)
                 const uint32_t cc = calls[tr.li];
                 const bool buf1 = Lp.ctr_mode == 2 ? (cc & 1u) : Lp.ctr_mode == 1 ? ((cc - 1u) & 1u) : false;
-                const CUtensorMap* tmA = buf1 ? &Lp.tmA1 : &Lp.tmA;
-                const CUtensorMap* tmB = buf1 ? &Lp.tmB1 : &Lp.tmB;
+                const CUtensorMap* tmA = &Lp.tmA;
+                const CUtensorMap* tmB = &Lp.tmB;
+                const int krow = buf1 ? Lp.kbuf : 0;     // the buffer's first row in the maps
                 const int nkb = gp.L[tr.li].num_k_blocks;
                 for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait(bar_empty + 8 * stage, phase ^ 1);
@@ -467,28 +465,28 @@ recon_tc_kernel(const __grid_constant__ GroupParams gp, const int npeers, const 
                         else ptx::mbar_arrive_cluster(fbl);
                         if (gp.L[tr.li].box3) {
                             // all MN chunks of an operand in one 3-D request (16 KB each)
-                            ptx::tma_load_3d_cg2(sa, tmA, fbl, 0, kb * C::BK, am0 / C::ELEMS);
-                            ptx::tma_load_3d_cg2(sb, tmB, fbl, 0, kb * C::BK, bn0 / C::ELEMS);
+                            ptx::tma_load_3d_cg2(sa, tmA, fbl, 0, kb * C::BK + krow, am0 / C::ELEMS);
+                            ptx::tma_load_3d_cg2(sb, tmB, fbl, 0, kb * C::BK + krow, bn0 / C::ELEMS);
                             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                             continue;
                         }
 #pragma unroll
                         for (int c = 0; c < C::A_CHUNKS; ++c)
-                            ptx::tma_load_2d_cg2(sa + c * C::CHUNK_BYTES, tmA, fbl, am0 + C::ELEMS * c, kb * C::BK);
+                            ptx::tma_load_2d_cg2(sa + c * C::CHUNK_BYTES, tmA, fbl, am0 + C::ELEMS * c, kb * C::BK + krow);
 #pragma unroll
                         for (int c = 0; c < C::B_CHUNKS; ++c)
-                            ptx::tma_load_2d_cg2(sb + c * C::CHUNK_BYTES, tmB, fbl, bn0 + C::ELEMS * c, kb * C::BK);
+                            ptx::tma_load_2d_cg2(sb + c * C::CHUNK_BYTES, tmB, fbl, bn0 + C::ELEMS * c, kb * C::BK + krow);
                     } else {
                         ptx::mbar_arrive_expect_tx(fb, C::STAGE_BYTES);
                         if (!X3 && gp.L[tr.li].box3) {
-                            ptx::tma_load_3d(sa, tmA, fb, 0, kb * C::BK, am0 / C::ELEMS);
-                            ptx::tma_load_3d(sb, tmB, fb, 0, kb * C::BK, bn0 / C::ELEMS);
+                            ptx::tma_load_3d(sa, tmA, fb, 0, kb * C::BK + krow, am0 / C::ELEMS);
+                            ptx::tma_load_3d(sb, tmB, fb, 0, kb * C::BK + krow, bn0 / C::ELEMS);
                             if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                             continue;
                         }
 #pragma unroll
                         for (int h = 0; h < C::HALVES; ++h) {     // X3: h = 1 loads the lo rows
-                            const int kr = kb * C::BK + h * gp.L[tr.li].k_lo;
+                            const int kr = kb * C::BK + h * gp.L[tr.li].k_lo + krow;
 #pragma unroll
                             for (int c = 0; c < C::A_CHUNKS; ++c)
                                 ptx::tma_load_2d(sa + (h * C::A_CHUNKS + c) * C::CHUNK_BYTES, tmA, fb,
@@ -998,11 +996,10 @@ bool big_tiles(const ReconArgs* a, int count) {
     return tiles_for(a, count, 256, ctas) >= num_sms() / ctas;
 }
 
-template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3 = false,
-          bool LONGK = false>
-tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
+template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3, bool LONGK, int MAXL>
+tag_status_t launch_m(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
     using C = Cfg<BN, CTAS, X3, (OUT_BF16 || X3 ? 1 : (SGD ? EXP_SGD_EP : 2)), LONGK>;
-    GroupParams gp;
+    GroupParamsT<MAXL> gp;
     std::memset(&gp, 0, sizeof gp);
     int tiles = 0;
     for (int i = 0; i < count; ++i) {
@@ -1016,24 +1013,21 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
             // an empty row shard (sharded sync, more ranks than 128-row tiles): no tiles and no
             // tensor maps; in a FUSED launch the layer's factors are still pushed to the peers
         } else {
-            // buffer 0 (or the only buffer), and for window operands buffer 1 as well
-            for (int buf = 0; buf < (a[i].ctr_mode ? 2 : 1); ++buf) {
-                CUtensorMap* mA = buf ? &L.tmA1 : &L.tmA;
-                CUtensorMap* mB = buf ? &L.tmB1 : &L.tmB;
-                const void* pA = buf ? a[i].A1 : a[i].A;
-                const void* pB = buf ? a[i].Bm1 : a[i].Bm;
-                if (L.box3) {
-                    if (!encode_3d(mA, pA, orows, a[i].M, C::BK, C::A_CHUNKS, a[i].lda) ||
-                        !encode_3d(mB, pB, orows, a[i].N, C::BK, C::B_CHUNKS))
-                        return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed for the factor operands");
-                } else if (!encode_2d(mA, pA, odt, oes, orows, a[i].M, C::ELEMS, C::BK, a[i].lda, oswz) ||
-                           !encode_2d(mB, pB, odt, oes, orows, a[i].N, C::ELEMS, C::BK, 0, oswz)) {
-                    return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
-                }
+            // window operands: one map over both buffers (2 * kbuf rows; rows K..kbuf of each
+            // buffer stay zero, so the last K block of buffer 0 never reads buffer 1)
+            const int64_t rows = a[i].ctr_mode && a[i].ctr ? 2 * a[i].kbuf : orows;
+            if (L.box3) {
+                if (!encode_3d(&L.tmA, a[i].A, rows, a[i].M, C::BK, C::A_CHUNKS, a[i].lda) ||
+                    !encode_3d(&L.tmB, a[i].Bm, rows, a[i].N, C::BK, C::B_CHUNKS))
+                    return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled (3-D) failed for the factor operands");
+            } else if (!encode_2d(&L.tmA, a[i].A, odt, oes, rows, a[i].M, C::ELEMS, C::BK, a[i].lda, oswz) ||
+                       !encode_2d(&L.tmB, a[i].Bm, odt, oes, rows, a[i].N, C::ELEMS, C::BK, 0, oswz)) {
+                return fail(TAG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the factor operands");
             }
         }
         L.ctr = a[i].ctr;
         L.ctr_mode = a[i].ctr ? a[i].ctr_mode : 0;
+        L.kbuf = static_cast<int>(a[i].kbuf);
         L.k_lo = X3 ? static_cast<int>(a[i].kpad) : 0;
         L.C = a[i].C;
         L.W = a[i].W;
@@ -1057,7 +1051,8 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
             L.win = static_cast<ncclWindow_t>(a[i].win);
             L.off_x = a[i].off_x;
             L.off_dy = a[i].off_dy;
-            L.buf_bytes = a[i].buf_bytes;
+            L.xbuf = a[i].xbuf;
+            L.ybuf = a[i].ybuf;
             L.off_flag = a[i].off_flag;
             L.flags = a[i].flags;
             L.vx = a[i].cx * 2 / 16;
@@ -1076,7 +1071,7 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
     gp.mc_base = FUSED ? static_cast<char*>(fg->mc_base) : nullptr;
     gp.cast = FUSED && fg->cast ? 1 : 0;
     gp.local_ctr = FUSED ? fg->local_ctr : nullptr;
-    auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED, X3, LONGK>;
+    auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED, X3, LONGK, MAXL>;
     // the shared-memory opt-in, once per instantiation and device (thread-safe)
     static std::atomic<uint64_t> attr_set{0};
     int dev = 0;
@@ -1139,6 +1134,13 @@ tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const Fused
 #endif
     count_launch();
     return TAG_OK;
+}
+
+template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3 = false,
+          bool LONGK = false>
+tag_status_t launch_t(const ReconArgs* a, int count, cudaStream_t s, const FusedGather* fg) {
+    if (count <= 4) return launch_m<BN, CTAS, OUT_BF16, SGD, FUSED, X3, LONGK, 4>(a, count, s, fg);
+    return launch_m<BN, CTAS, OUT_BF16, SGD, FUSED, X3, LONGK, MAX_GROUP>(a, count, s, fg);
 }
 
 template <bool FUSED>

@@ -58,10 +58,13 @@ __device__ __forceinline__ uint32_t load_calls(const uint32_t* ctr) {
 struct ReconArgs {
     const void* A;       // K x M
     const void* Bm;      // K x N
-    // window operands: A / Bm are buffer 0, A1 / Bm1 buffer 1, ctr the window's call counter;
-    // ctr_mode 1: read the latest gather ((c - 1) & 1), 2: the fused kernel's own (c & 1)
+    // window operands: A / Bm are buffer 0 and buffer 1 starts kbuf rows further (the window
+    // holds [X buf 0 | X buf 1 | dY buf 0 | dY buf 1], each buffer kbuf rows, zero beyond K), A1 /
+    // Bm1 point at it; ctr is the window's call counter; ctr_mode 1: read the latest gather's
+    // buffer ((c - 1) & 1), 2: the fused kernel's own (c & 1)
     const void* A1;
     const void* Bm1;
+    int64_t kbuf;
     const uint32_t* ctr;
     int ctr_mode;
     void* C;             // M x N, out dtype; may be nullptr when sgd (no dW write)
@@ -85,8 +88,8 @@ struct ReconArgs {
     const void* srcX;      // X_r, dY_r (in dtype: wire dtype, or fp32 with FusedGather::cast)
     const void* srcY;
     void* win;             // ncclWindow_t of the layer's symmetric window
-    uint64_t off_x, off_dy;  // buffer 0's X_all / dY_all in the window (buffer 1: + buf_bytes)
-    uint64_t buf_bytes;
+    uint64_t off_x, off_dy;  // buffer 0's X_all / dY_all in the window
+    uint64_t xbuf, ybuf;     // buffer 1's X_all / dY_all are xbuf / ybuf bytes further
     uint64_t off_flag;     // the window flag area (WIN_* offsets)
     uint32_t* flags;       // the same area, this rank's device address
     int64_t cx, cy;        // elements of X_r / dY_r
@@ -129,7 +132,7 @@ struct PushSegment {
     const void* dY;
     void* win;              // ncclWindow_t
     size_t off_x, off_dy;   // byte offsets of buffer 0's X_all / dY_all in the window
-    size_t buf_bytes;       // buffer 1 = buffer 0 + buf_bytes
+    size_t xbuf, ybuf;      // buffer 1's X_all / dY_all are xbuf / ybuf bytes further
     size_t off_flag;        // the window flag area (WIN_* offsets)
     uint32_t* flags;        // the same area, this rank's device address
     int64_t cx, cy;         // elements of this rank's X_r / dY_r
