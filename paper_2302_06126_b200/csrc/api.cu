@@ -25,6 +25,9 @@ bool push_devcomm_all_lsa(const void* dc, int nranks);
 void* push_devcomm_mc_base(const void* dc);
 tag_status_t launch_comm_barrier(const void* dc, int index, cudaStream_t s);
 constexpr int PUSH_MAX_CTAS = 148;
+#ifndef EXP_PUSH_GRID
+#define EXP_PUSH_GRID PUSH_MAX_CTAS   // diagnostics builds: cap on the push kernel's grid
+#endif
 constexpr int COMM_BARRIER_INDEX = PUSH_MAX_CTAS;   // LSA barrier slot of tag_comm_barrier
 
 std::atomic<uint64_t> g_launches{0};
@@ -282,7 +285,7 @@ tag_status_t do_gather(tag_plan_s* p, const void* X, const void* dY, cudaStream_
         // kernel picks the buffer from the window's call counter and advances it
         PushSegment seg = push_segment(p, X, dY);
         TAG_TRY(launch_push_gather_group(p->comm->devcomm, &seg, 1, r, d.in_dtype, d.wire_dtype,
-                                         PUSH_MAX_CTAS, p->flags + WIN_LOCAL_PUSH / 4, s));
+                                         EXP_PUSH_GRID, p->flags + WIN_LOCAL_PUSH / 4, s));
         set_src_window(p);
         return TAG_OK;
     }
@@ -1138,7 +1141,7 @@ tag_status_t tag_sfb_group_gather(tag_sfb_group_t g, const void* const* X, const
         for (int i = 0; i < count; ++i) seg[i] = push_segment(g->plans[i], X[i], dY[i]);
         tag_plan_s* p0 = g->plans[0];
         TAG_TRY(launch_push_gather_group(c->devcomm, seg, count, c->rank, p0->d.in_dtype,
-                                         p0->d.wire_dtype, PUSH_MAX_CTAS, p0->flags + WIN_LOCAL_PUSH / 4, s));
+                                         p0->d.wire_dtype, EXP_PUSH_GRID, p0->flags + WIN_LOCAL_PUSH / 4, s));
         for (int i = 0; i < count; ++i) set_src_window(g->plans[i]);
         return TAG_OK;
     }

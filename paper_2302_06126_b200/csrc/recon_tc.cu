@@ -947,8 +947,11 @@ bool encode_3d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int 
 
 // one CTA (pair) per SM (TPC), at most one per tile; a FUSED launch keeps at least one unit even
 // with no tiles (every rank must push its factors)
+#ifndef EXP_RECON_SMS
+#define EXP_RECON_SMS 0   // diagnostics builds: SMs the persistent grid may use (0 = all)
+#endif
 int grid_for(int tiles, int ctas, bool fused) {
-    const int units = num_sms() / ctas;
+    const int units = (EXP_RECON_SMS ? EXP_RECON_SMS : num_sms()) / ctas;
     int g = tiles < units ? tiles : units;
     if (fused && g < 1) g = 1;
     return ctas * g;
