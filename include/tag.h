@@ -272,6 +272,12 @@ tag_status_t tag_sfb_sync_sharded(tag_sfb_plan_t plan, const void* X, const void
  * Errors: TAG_ERR_INVALID_ARG (plan without fuse_sgd, NULL / misaligned pointers). */
 tag_status_t tag_sfb_sync_sharded_sgd(tag_sfb_plan_t plan, const void* X, const void* dY, float* W,
                                       float* v_shard, tag_stream_t stream);
+/* COLLECTIVE (n > 1). The same with Adam (desc.fuse_adam = 1, step t >= 1, R22): m_shard and
+ * v_shard are this rank's row_count x N moment rows; W after the call is bitwise equal to
+ * tag_sfb_sync_adam's on every rank. */
+tag_status_t tag_sfb_sync_sharded_adam(tag_sfb_plan_t plan, const void* X, const void* dY, float* W,
+                                       float* m_shard, float* v_shard, int64_t step,
+                                       tag_stream_t stream);
 
 /* Bias gradient of the layer (y = x W + b; DESIGN R17): db = alpha * sum_k dY_all[k][:], the
  * column sums of the gathered output gradients — the bias is the weight of a constant input, so

@@ -929,26 +929,25 @@ tag_status_t allgather_rows(tag_plan_s* p, float* W, cudaStream_t s) {
     return e == ncclSuccess ? TAG_OK : nccl_fail(e, "ncclGroupEnd");
 }
 
-tag_status_t tag_sfb_sync_sharded_sgd(tag_sfb_plan_t p, const void* X, const void* dY, float* W,
-                                      float* v_shard, tag_stream_t stream) {
-    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_sgd: NULL plan");
-    if (!p->d.fuse_sgd) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_sgd: plan has fuse_sgd = 0");
-    if (p->d.out_dtype != TAG_F32)
-        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_sgd: needs out_dtype = F32");
+// The sharded optimizer step (f-2, R24) for SGD-momentum (adam == nullptr) or Adam: this rank's
+// rows of W with its optimizer-state rows, then the W all-gather.
+static tag_status_t sharded_opt(tag_sfb_plan_t p, const void* X, const void* dY, float* W,
+                                float* m_shard, float* v_shard, const AdamCall* adam,
+                                tag_stream_t stream, const char* fn) {
+    if (p->d.out_dtype != TAG_F32) return fail(TAG_ERR_INVALID_ARG, std::string(fn) + ": needs out_dtype = F32");
     int64_t rb, rc;
     shard_range(p, p->comm->rank, &rb, &rc);
-    TAG_TRY(check_ptrs("tag_sfb_sync_sharded_sgd", {X, dY, W}));
-    if (rc > 0) TAG_TRY(check_ptrs("tag_sfb_sync_sharded_sgd", {v_shard}));
-    if (((rb * p->d.N * 4) & 15) != 0)
-        return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_sgd: shard rows not 16-byte aligned");
+    TAG_TRY(check_ptrs(fn, {X, dY, W}));
+    if (rc > 0) TAG_TRY(check_ptrs(fn, {v_shard}));
+    if (rc > 0 && adam) TAG_TRY(check_ptrs(fn, {m_shard}));
     TAG_TRY(set_device(p->comm));
     TAG_TRY(check_async(p->comm));
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    float* Ws = W + rb * p->d.N;               // this rank's rows of W
+    float* Ws = W + rb * p->d.N;               // this rank's rows of W (rb is a multiple of 128)
     void* none = nullptr;
-    if (fusable(p, nullptr, 1)) {
-        // one fused launch: push, reconstruct this rank's rows, SGD-momentum on them
-        TAG_TRY(fused_sync(&p, 1, &X, &dY, &none, true, &Ws, &v_shard, s, true));
+    if (fusable(p, nullptr, adam ? 2 : 1)) {
+        // one fused launch: push, reconstruct this rank's rows, the optimizer on them
+        TAG_TRY(fused_sync(&p, 1, &X, &dY, &none, true, &Ws, &v_shard, s, true, &m_shard, adam));
     } else {
         TAG_TRY(do_gather(p, X, dY, s));
         if (rc > 0) {
@@ -968,12 +967,49 @@ tag_status_t tag_sfb_sync_sharded_sgd(tag_sfb_plan_t p, const void* X, const voi
             a.lr = p->d.lr;
             a.mu = p->d.momentum;
             a.wd = p->d.weight_decay;
-            a.opt = 1;
-            TAG_TRY((p->use_tc && recon_tc_ok(a)) ? launch_recon_tc(a, s) : launch_recon_simt(a, s));
+            set_adam(a, m_shard, adam);
+            if (p->use_tc && recon_tc_ok(a)) {
+                TAG_TRY(launch_recon_tc(a, s));
+            } else if (!adam) {
+                TAG_TRY(launch_recon_simt(a, s));
+            } else {
+                // the SIMT kernel has no Adam epilogue: the shard's dW into the plan's staging,
+                // then the unfused Adam kernel on the shard (the same arithmetic, optim.cuh)
+                if (!p->adam_dw) {
+                    cudaError_t e = cudaMallocAsync(&p->adam_dw, static_cast<size_t>(p->d.M * p->d.N) * 4, s);
+                    if (e != cudaSuccess) {
+                        p->adam_dw = nullptr;
+                        return cuda_fail(e, "cudaMallocAsync(Adam staging)");
+                    }
+                }
+                a.C = p->adam_dw;
+                a.sgd = false;
+                TAG_TRY(launch_recon_simt(a, s));
+                TAG_TRY(launch_adam(p->adam_dw, Ws, m_shard, v_shard, rc * p->d.N, adam->b1, adam->omb1,
+                                    adam->b2, adam->omb2, adam->eps, adam->lr_t, adam->isbc2,
+                                    p->d.weight_decay, s));
+            }
         }
     }
     // parameter all-gather: every rank ends with the whole updated W (ZeRO-style)
     return allgather_rows(p, W, s);
+}
+
+tag_status_t tag_sfb_sync_sharded_sgd(tag_sfb_plan_t p, const void* X, const void* dY, float* W,
+                                      float* v_shard, tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_sgd: NULL plan");
+    if (!p->d.fuse_sgd) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_sgd: plan has fuse_sgd = 0");
+    return sharded_opt(p, X, dY, W, nullptr, v_shard, nullptr, stream, "tag_sfb_sync_sharded_sgd");
+}
+
+tag_status_t tag_sfb_sync_sharded_adam(tag_sfb_plan_t p, const void* X, const void* dY, float* W,
+                                       float* m_shard, float* v_shard, int64_t step,
+                                       tag_stream_t stream) {
+    if (!p) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_adam: NULL plan");
+    if (!p->d.fuse_adam) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_adam: plan has fuse_adam = 0");
+    if (step < 1) return fail(TAG_ERR_INVALID_ARG, "tag_sfb_sync_sharded_adam: step must be >= 1");
+    const AdamCall ad = adam_call(p->d, step);
+    return sharded_opt(p, X, dY, W, m_shard, v_shard, &ad, stream, "tag_sfb_sync_sharded_adam");
 }
 
 tag_status_t tag_sfb_sync_host(tag_sfb_plan_t p, const void* X_host, const void* dY_host,

@@ -107,6 +107,7 @@ _SIGS = {
     "tag_sfb_shard_rows": ([_vp, _i, _p(ctypes.c_int64), _p(ctypes.c_int64)], _st),
     "tag_sfb_sync_sharded": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_sfb_sync_sharded_sgd": ([_vp, _vp, _vp, _vp, _vp, _vp], _st),
+    "tag_sfb_sync_sharded_adam": ([_vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_int64, _vp], _st),
     "tag_local_grad": ([_vp, _vp, _vp, _vp, _vp], _st),
     "tag_dense_allreduce": ([_vp, _vp, _vp], _st),
     "tag_ps_sync": ([_vp, _vp, _i, _vp], _st),
@@ -338,6 +339,17 @@ class SfbPlan:
         _check(_lib.tag_sfb_sync_sharded_sgd(self._h, x, dy,
                                              self._dev(W, torch.float32, (self.M, self.N), "W"), v,
                                              _stream(stream)), "tag_sfb_sync_sharded_sgd")
+
+    def sync_sharded_adam(self, X, dY, W, m_shard, v_shard, step, stream=None):
+        """Sharded Adam on this rank's rows of W (moment rows m_shard, v_shard), then the W
+        all-gather."""
+        x, dy = self._xy(X, dY)
+        _, rc = self.shard_rows()
+        m = self._dev(m_shard, torch.float32, (rc, self.N), "m_shard") if rc > 0 else _vp()
+        v = self._dev(v_shard, torch.float32, (rc, self.N), "v_shard") if rc > 0 else _vp()
+        _check(_lib.tag_sfb_sync_sharded_adam(self._h, x, dy,
+                                              self._dev(W, torch.float32, (self.M, self.N), "W"), m, v,
+                                              step, _stream(stream)), "tag_sfb_sync_sharded_adam")
 
     def sync_host(self, X_host, dY_host, dW_host, stream=None):
         _check(_lib.tag_sfb_sync_host(

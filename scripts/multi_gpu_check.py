@@ -347,6 +347,30 @@ def main():
         plan.close()
     record("sharded_sgd_allgather", oks)
 
+    # 13b: the same with Adam (tag_sfb_sync_sharded_adam) against the replicated fused Adam
+    oka = True
+    for li, (M, N, B) in enumerate([(4096, 1024, 32), (96, 264, 32)]):
+        X, dY = synth.factors(69, li, rank, M, N, B, "normal", "small")
+        W0, _ = synth.sgd_state(69, li, M, N)
+        plan = tag.SfbPlan(comm, M, N, B, "bf16", "bf16", "f32", fuse_adam=True, lr=1e-3,
+                           weight_decay=0.01, gather=gather)
+        Xd, dYd = torch.from_numpy(X).to(torch.bfloat16).cuda(), torch.from_numpy(dY).to(torch.bfloat16).cuda()
+        Wr = torch.from_numpy(W0).cuda()
+        mr, vr = torch.zeros_like(Wr), torch.zeros_like(Wr)
+        rb, rc = plan.shard_rows()
+        Ws = Wr.clone()
+        ms = torch.zeros(max(rc, 1), N, device="cuda")[:rc]
+        vs = torch.zeros(max(rc, 1), N, device="cuda")[:rc]
+        for t in (1, 2, 3):
+            plan.sync_adam(Xd, dYd, Wr, mr, vr, t)
+            plan.sync_sharded_adam(Xd, dYd, Ws, ms, vs, t)
+        torch.cuda.synchronize()
+        hashes = tdist.all_gather_object(digest(Ws))
+        oka = oka and torch.equal(Ws, Wr) and torch.equal(ms, mr[rb:rb + rc]) and \
+            torch.equal(vs, vr[rb:rb + rc]) and len(set(hashes)) == 1
+        plan.close()
+    record("sharded_adam_allgather", oka)
+
     # 14: full-size layers through the bench's launch configuration at this n — VGG-19 fc6
     #     (25088 x 4096, B = 32; fused push, K = 32n) and the Transformer output projection
     #     (512 x 32000, 256 tokens; K = 256n, column-sweep raster) — 4000 entries per layer against

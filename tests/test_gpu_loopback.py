@@ -418,3 +418,21 @@ def test_cuda_graph_capture_exchange(tag, loop, oracle_mod):
     g.close()
     for p in plans:
         p.close()
+
+
+def test_sharded_adam_with_parameter_allgather(tag, loop):
+    """f-2 with Adam on one rank (loopback): == the replicated fused Adam bit for bit, 3 steps."""
+    M, N, B = 520, 264, 24
+    X, dY = synth.factors(69, 1, 0, M, N, B, "normal", "small")
+    W0, _ = synth.sgd_state(69, 1, M, N)
+    plan = tag.SfbPlan(loop, M, N, B, fuse_adam=True, lr=1e-3, weight_decay=0.01)
+    Xd, dYd = dev(X, "bf16"), dev(dY, "bf16")
+    Wr = torch.from_numpy(W0).cuda()
+    mr, vr = torch.zeros_like(Wr), torch.zeros_like(Wr)
+    Ws, ms, vs = Wr.clone(), mr.clone(), vr.clone()
+    for t in (1, 2, 3):
+        plan.sync_adam(Xd, dYd, Wr, mr, vr, t)
+        plan.sync_sharded_adam(Xd, dYd, Ws, ms, vs, t)
+    torch.cuda.synchronize()
+    assert torch.equal(Ws, Wr) and torch.equal(ms, mr) and torch.equal(vs, vr)
+    plan.close()
