@@ -608,6 +608,34 @@ def main():
                    "dW_GBps_all_ranks": round(dw_bytes / (t_sh * 1e-3) / 1e9, 1),
                    "note": "each rank reconstructs M/n rows of every layer (tag_sfb_group_sync_sharded)"}
 
+    # f-2 for the fused-optimizer configs: the sharded SGD step (each rank updates its rows of W
+    # and its momentum shard in the fused launch) + the W all-gather, per layer in sequence,
+    # against the replicated fused SGD of the same layers (the headline step)
+    if n > 1 and cfg.sgd:
+        vsh = []
+        for l in layers:
+            rb, rc = l["plan"].shard_rows()
+            vsh.append(torch.zeros(max(rc, 1), l["L"].N, device="cuda")[:rc])
+
+        def sharded_sgd_step():
+            with torch.cuda.stream(stream):
+                for l, v in zip(layers, vsh):
+                    l["plan"].sync_sharded_sgd(l["X"], l["dY"], l["W"], v, stream)
+        for _ in range(3):
+            sharded_sgd_step()
+        ts = []
+        for _ in range(max(5, min(args.steps, 20))):
+            e0, e1 = start_events(2)
+            sharded_sgd_step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        t_sh = tdist.max_over_ranks(statistics.mean(ts))
+        sharded = {"ms_per_step": round(t_sh, 4),
+                   "replicated_fused_sgd_ms": round(t_step_ms, 4),
+                   "note": "tag_sfb_sync_sharded_sgd per layer: sharded SGD-momentum in the fused "
+                           "launch + W all-gather (momentum memory / n)"}
+
     # ---------------------------------------------------------------- e2e through host buffers
     dWh = [torch.empty(l["L"].M, l["L"].N, dtype=tdt[cfg.out_dtype]).pin_memory() for l in layers]
     h2d = sum(l["Xh"].numel() * l["Xh"].element_size() + l["dYh"].numel() * l["dYh"].element_size()
