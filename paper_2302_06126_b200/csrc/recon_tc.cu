@@ -587,12 +587,12 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
             const int n0 = tr.n0;
             const int row0 = tr.m0 + static_cast<int>(crank) * BM + 32 * quad;  // first row
 #ifndef EXP_OPT_PREFETCH
-#define EXP_OPT_PREFETCH 1
+#define EXP_OPT_PREFETCH 0
 #endif
             if constexpr (SGD && EXP_OPT_PREFETCH) {
-                // The optimizer state this warp will update does not depend on the MMA: pull its
-                // rows (one per lane, GC columns) into L2 while the accumulator is still being
-                // computed, so the epilogue's W / v (/ m) loads hit L2 instead of HBM latency.
+                // Diagnostics builds (the round-1 product, before the hoisted loads below): pull
+                // this warp's rows of the optimizer state into L2 while the accumulator is still
+                // being computed. With the loads hoisted it costs 1-2 us on the BERT-L bucket.
                 auto prefetch_tile = [&](int t) {
                     const TileRef pr = locate<BN, CTAS>(gp, t);
                     const LayerParams& pl = gp.L[pr.li];
@@ -611,14 +611,28 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
                 if (EXP_OPT_PREFETCH == 1 || tile == unit) prefetch_tile(tile);
                 if (EXP_OPT_PREFETCH == 2 && tile + nunits < gp.num_tiles) prefetch_tile(tile + nunits);
             }
-            ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
-            ptx::tc_fence_after();
+#ifndef EXP_OPT_HOIST
+#define EXP_OPT_HOIST 1
+#endif
+            // HOIST: the optimizer state of a full chunk does not depend on the accumulator —
+            // all 8 rows' loads (per lane) are issued before the accumulator wait / TMEM read /
+            // transpose, so their latency overlaps those and the Adam math of the previous chunk
+            // (measured, scripts/opt_epilogue_ab.py: Adam 59.5 -> 48.0 us on the BERT-L bucket)
+            constexpr bool HOIST = SGD && EXP_OPT_HOIST;
+            if (!HOIST) {
+                ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
+                ptx::tc_fence_after();
+            }
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(32 * quad) << 16) + acc * C::ACC_COLS;
             // chunks of this warp's column half that hold any output column (warp-uniform)
             int nch = (N - (n0 + half * GC) + COLS_PER_CHUNK - 1) / COLS_PER_CHUNK;
             nch = nch < 0 ? 0 : (nch > CHUNKS ? CHUNKS : nch);
             if (EXP_EPI_MODE == 2) nch = 0;
             if (nch == 0) {                       // nothing to read: release the accumulator
+                if (HOIST) {
+                    ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
+                    ptx::tc_fence_after();
+                }
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
@@ -629,6 +643,32 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
 #pragma unroll 1
             for (int ch = 0; ch < nch; ch += PAIR) {
                 const int np = (nch - ch) < PAIR ? (nch - ch) : PAIR;    // chunks this round
+                [[maybe_unused]] float4 hw[8], hv[8], hm[8];
+                [[maybe_unused]] const bool hfull =
+                    row0 + 32 <= M && n0 + half * GC + (ch + 1) * COLS_PER_CHUNK <= N;
+                if constexpr (HOIST) {
+                    if (hfull) {
+                        const int64_t o = static_cast<int64_t>(row0 + sub) * N + n0 + half * GC +
+                                          ch * COLS_PER_CHUNK + cj * VEC;
+                        const float4* wp4 = reinterpret_cast<const float4*>(Wp + o);
+                        const float4* vp4 = reinterpret_cast<const float4*>(Vp + o);
+                        const int64_t gs = static_cast<int64_t>(N);          // 4 rows, in float4
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            hw[i] = __ldcs(wp4 + i * gs);
+                            hv[i] = __ldcs(vp4 + i * gs);
+                        }
+                        if (gp.opt == 2) {
+                            const float4* mp4 = reinterpret_cast<const float4*>(lp.Mm + o);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) hm[i] = __ldcs(mp4 + i * gs);
+                        }
+                    }
+                    if (ch == 0) {
+                        ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
+                        ptx::tc_fence_after();
+                    }
+                }
                 uint32_t w[PAIR][32];                                    // 128 B of row per chunk
                 // ---- TMEM -> registers: every load of the round issued before one wait
 #pragma unroll
@@ -772,9 +812,15 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
 #pragma unroll
                                 for (int i = 0; i < 4; ++i) {
                                     const int r = 4 * hh + i;
-                                    wv[i] = __ldcs(wp4 + r * gstep);
-                                    mv[i] = __ldcs(mp4 + r * gstep);
-                                    vv[i] = __ldcs(vp4 + r * gstep);
+                                    if constexpr (HOIST) {
+                                        wv[i] = hw[r];
+                                        mv[i] = hm[r];
+                                        vv[i] = hv[r];
+                                    } else {
+                                        wv[i] = __ldcs(wp4 + r * gstep);
+                                        mv[i] = __ldcs(mp4 + r * gstep);
+                                        vv[i] = __ldcs(vp4 + r * gstep);
+                                    }
                                 }
 #pragma unroll
                                 for (int i = 0; i < 4; ++i) {
@@ -814,8 +860,13 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
                             float4 wv[RW], vv[RW];
 #pragma unroll
                             for (int i = 0; i < RW; ++i) {
-                                wv[i] = __ldcs(wp4 + (h0 + i) * gstep);
-                                vv[i] = __ldcs(vp4 + (h0 + i) * gstep);
+                                if constexpr (HOIST) {
+                                    wv[i] = hw[h0 + i];
+                                    vv[i] = hv[h0 + i];
+                                } else {
+                                    wv[i] = __ldcs(wp4 + (h0 + i) * gstep);
+                                    vv[i] = __ldcs(vp4 + (h0 + i) * gstep);
+                                }
                             }
 #pragma unroll
                             for (int ii = 0; ii < RW; ++ii) {
