@@ -201,13 +201,36 @@ def virtual_n_recon(tag, comm, cfg, nv, stream, flush_l2, start_events, peaks, i
                 torch.cuda.synchronize()
                 ts.append(evs[0].elapsed_time(evs[1]))
             t = statistics.median(ts) * 1e-3
+            # the same launch replayed back to back from CUDA graphs (1 and 10 launches, L2 flushed
+            # before each replay): the slope is the per-launch device time without the ~2.5 us
+            # CUDA-event floor and the launch gap a single-launch interval carries
+            # (scripts/event_floor.py); the 10 launches rewrite the same dW, factors stay in L2
+            graphs = {}
+            for reps in (1, 10):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for _ in range(reps):
+                        plan.reconstruct(dW, stream)
+                graphs[reps] = g
+            gts = {1: [], 10: []}
+            for _ in range(iters):
+                for reps in (1, 10):
+                    evs = start_events(2)
+                    with torch.cuda.stream(stream):
+                        graphs[reps].replay()
+                    evs[1].record(stream)
+                    torch.cuda.synchronize()
+                    gts[reps].append(evs[0].elapsed_time(evs[1]))
+            t_b2b = (statistics.median(gts[10]) - statistics.median(gts[1])) / 9 * 1e-3
             flops = 2.0 * L.M * L.N * K
             byts = K * (L.M + L.N) * 2 + L.M * L.N * ESIZE[out_dt]
             res[L.name] = {"K": K, "us": round(t * 1e6, 2),
                            "tensor_frac": round(flops / t / 1e12 / peaks["bf16_tflops"], 4),
                            "hbm_frac": round(byts / t / 1e9 / peaks["hbm_gbs"], 4),
                            "ideal_tensor_us": round(flops / (peaks["bf16_tflops"] * 1e12) * 1e6, 2),
-                           "ideal_hbm_us": round(byts / (peaks["hbm_gbs"] * 1e9) * 1e6, 2)}
+                           "ideal_hbm_us": round(byts / (peaks["hbm_gbs"] * 1e9) * 1e6, 2),
+                           "us_per_launch_b2b": round(t_b2b * 1e6, 2),
+                           "tensor_frac_b2b": round(flops / t_b2b / 1e12 / peaks["bf16_tflops"], 4)}
             plan.close()
         out[f"dW_{out_dt}"] = res
     return out
