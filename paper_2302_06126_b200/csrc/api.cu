@@ -128,6 +128,8 @@ struct tag_plan_s {
     int64_t kpad = 0;
     // Adam on a path without the fused epilogue: dW staged here, then the unfused Adam kernel
     float* adam_dw = nullptr;
+    // the reconstruction kernel's dynamic tile-schedule counters (recon_tc.cu), zeroed once
+    uint32_t* sched = nullptr;
 };
 
 struct tag_group_s {
@@ -234,6 +236,7 @@ void set_src_window(tag_plan_s* p) {
 // a's operands from the plan's latest gather; columns col0.. of X_all (sharded rows of dW)
 void fill_src(const tag_plan_s* p, ReconArgs& a, int64_t col0 = 0) {
     const size_t xo = static_cast<size_t>(col0) * dtype_size(p->d.wire_dtype);
+    a.sched = p->sched;
     a.A = static_cast<const char*>(p->src_x) + xo;
     a.Bm = p->src_dy;
     if (p->src_ctr) {
@@ -643,6 +646,7 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
                  (!EXP_F32_SIMT && static_cast<int64_t>(d->n) * d->B <= 4096));
     auto cleanup = [p]() {
         cudaFree(p->split);
+        cudaFree(p->sched);
         cudaFree(p->gx);
         cudaFree(p->gdy);
         cudaFree(p->lx);
@@ -707,6 +711,14 @@ tag_status_t tag_sfb_plan(tag_comm_t c, const tag_sfb_desc_t* d, tag_sfb_plan_t*
         if (e != cudaSuccess) {
             cleanup();
             return cuda_fail(e, "tag_sfb_plan: cudaMalloc(gather buffers)");
+        }
+    }
+    if (p->use_tc) {
+        cudaError_t e = cudaMalloc(&p->sched, 64);
+        if (e == cudaSuccess) e = cudaMemset(p->sched, 0, 64);
+        if (e != cudaSuccess) {
+            cleanup();
+            return cuda_fail(e, "tag_sfb_plan: cudaMalloc(tile schedule counters)");
         }
     }
     if (p->use_tc && d->wire_dtype == TAG_F32) {
@@ -774,6 +786,7 @@ tag_status_t tag_sfb_plan_destroy(tag_sfb_plan_t p) {
     cudaFree(p->st_dy);
     cudaFree(p->st_dw);
     cudaFree(p->split);
+    cudaFree(p->sched);
     delete p;
     return TAG_OK;
 }

@@ -28,11 +28,14 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <atomic>
+#include <climits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include <nccl.h>
 #include <nccl_device.h>
@@ -54,6 +57,7 @@ constexpr int NUM_THREADS = 64 + 32 * NUM_EPI_WARPS;   // 320
 constexpr int EPI_CHUNK_BYTES = 32 * 128;    // one 32 rows x 128 B transpose buffer
 constexpr int SMEM_MAX = 232448;              // 227 KB of dynamic shared memory per CTA
 constexpr int TMEM_COLS = 512;
+constexpr int SCHED_RING = 16;               // tile ids in flight between the producer and consumers
 // Diagnostics only (scripts/build_variant.sh, never the product build): 1 = epilogue skips the
 // global stores, 2 = epilogue releases each accumulator without reading it
 #ifndef EXP_SGD_EP
@@ -118,7 +122,9 @@ struct Cfg {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int EPI_BUF_BYTES = EP * EPI_CHUNK_BYTES;   // per epilogue warp
     static constexpr int EPI_BYTES = NUM_EPI_WARPS * EPI_BUF_BYTES;
-    static constexpr int BAR_BYTES = 256;
+    // mbarriers + TMEM slot (< 256 B), the tile-schedule ring at +512 (SCHED_RING full / empty
+    // barriers and tile ids)
+    static constexpr int BAR_BYTES = 1024;
     // as many stages as fit, at most 8 (BN = 128: 8; BN = 256 one CTA: 6; pairs: 3 with a
     // one-chunk epilogue, 2 with the two-chunk fp32 one)
     static constexpr int FIT = (SMEM_MAX - 1024 - EPI_BYTES - BAR_BYTES) / STAGE_BYTES;
@@ -179,6 +185,9 @@ struct GroupParamsT {
     char* mc_base;         // FUSED: NVLS multicast base of the windows, or nullptr (unicast)
     int cast;              // FUSED: the sources are fp32, cast to bf16 (RNE) on the way out
     uint32_t* local_ctr;   // FUSED: self-resetting hierarchical publish counter
+    // dynamic tile schedule (one-CTA tiles): [next-tile counter, finished-CTA counter], zero
+    // between launches (the last CTA to finish resets both); nullptr = static round robin
+    uint32_t* sched;
 };
 
 struct TileRef {
@@ -230,7 +239,16 @@ __device__ __forceinline__ void* mc_ptr(char* mc_base, ncclWindow_t w, size_t of
     return mc_base + static_cast<size_t>(w->mcOffset4K) * 4096 + off;
 }
 
-#if EXP_FUSED_DBG == 3
+#ifndef EXP_STATIC_SCHED
+#define EXP_STATIC_SCHED 0   // diagnostics builds: the static round-robin tile schedule everywhere
+#endif
+#ifndef EXP_DYN_WAVES
+#define EXP_DYN_WAVES 2      // rounds of tiles at the end handed out dynamically
+#endif
+#ifndef EXP_END_STAMPS
+#define EXP_END_STAMPS 0   // diagnostics builds: per-CTA start / end stamps of every launch
+#endif
+#if EXP_FUSED_DBG == 3 || EXP_END_STAMPS
 // diagnostics builds: per-CTA %globaltimer stamps [cta][slot] — 0 start, 1 push stores issued,
 // 2 CTA barrier, 3 system-scope fence, 4 local counter add, 5 (last CTA of the rank) second fence +
 // remote adds, 6 first arrival wait satisfied, 7 end — printed by the host after each launch
@@ -376,15 +394,37 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
     const uint32_t bar_tfull = s_bar + 16 * C::STAGES;     // [ACC]
     const uint32_t bar_tempty = bar_tfull + 8 * C::ACC;    // [ACC]
     const uint32_t s_tmem_slot = bar_tempty + 8 * C::ACC;
+    // dynamic tile schedule (one-CTA tiles, gp.sched set): the producer takes each CTA's next
+    // tile from a global counter and hands it to the MMA issuer and the epilogue warps through a
+    // SCHED_RING-deep smem ring (full: 1 arrival, empty: the MMA thread + every epilogue warp)
+    const bool dyn = CTAS == 1 && gp.sched != nullptr;
+    const uint32_t sch_full = s_bar + 512;                 // [SCHED_RING]
+    const uint32_t sch_empty = sch_full + 8 * SCHED_RING;  // [SCHED_RING]
+    const uint32_t s_sch = sch_empty + 8 * SCHED_RING;     // int [SCHED_RING]
     uint8_t* gen_base = smem_raw + (base - ptx::smem_addr(smem_raw));
     volatile uint32_t* tmem_slot_ptr =
         reinterpret_cast<volatile uint32_t*>(gen_base + (s_tmem_slot - base));
+    const int unit = blockIdx.x / CTAS;      // this CTA's (pair's) index in the tile schedule
+    const int nunits = gridDim.x / CTAS;
+    volatile int* sch = reinterpret_cast<volatile int*>(gen_base + (s_sch - base));
+    // the j-th tile of this CTA (-1: none left) for the MMA issuer (one thread) or an epilogue
+    // warp (whole warp: every lane reads the slot before lane 0 frees it)
+    auto next_tile = [&](int j, bool whole_warp) -> int {
+        if (!dyn) {
+            const int t = unit + j * nunits;
+            return t < gp.num_tiles ? t : -1;
+        }
+        const int r = j % SCHED_RING;
+        ptx::mbar_wait(sch_full + 8 * r, (j / SCHED_RING) & 1);
+        const int t = sch[r];
+        if (whole_warp) __syncwarp();
+        if (!whole_warp || ptx::lane_id() == 0) ptx::mbar_arrive(sch_empty + 8 * r);
+        return t;
+    };
 
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t crank = CTAS == 2 ? ptx::cluster_ctarank() : 0;   // 0 = leader of the pair
-    const int unit = blockIdx.x / CTAS;      // this CTA's (pair's) index in the tile schedule
-    const int nunits = gridDim.x / CTAS;
 
     // ---- prologue (overlaps the previous kernel's tail under programmatic dependent launch)
     if (warp == 0 && lane == 0) {
@@ -401,6 +441,11 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
             ptx::mbar_init(bar_tfull + 8 * a, 1);
             ptx::mbar_init(bar_tempty + 8 * a, NUM_EPI_WARPS * CTAS);   // pair: both CTAs drain
         }
+        if (dyn)
+            for (int r = 0; r < SCHED_RING; ++r) {
+                ptx::mbar_init(sch_full + 8 * r, 1);
+                ptx::mbar_init(sch_empty + 8 * r, 1 + NUM_EPI_WARPS);
+            }
         ptx::fence_mbar_init();
     }
     if (warp == 1) {
@@ -414,6 +459,7 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
     const uint32_t tmem_base = *tmem_slot_ptr;
     // no global memory is touched before the previous grid in the stream has completed
     grid_dep_wait();
+    if (EXP_END_STAMPS && threadIdx.x == 0) DBG_STAMP(0);
     // Diagnostics builds only (scripts/build_variant.sh -DEXP_FUSED_DBG=k, never the product):
     // 1 = no push and no wait, 2 = push without the arrival wait, 3 = phase stamps.
     uint32_t calls[MAXL];                     // window operands: each layer's call counter c
@@ -428,7 +474,33 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
             int stage = 0;
             uint32_t phase = 0;
             uint32_t ready = 0;               // layers whose call counter (and, FUSED, factors) are known
-            for (int tile = unit; tile < gp.num_tiles; tile += nunits) {
+            // dyn: the first W - 2 rounds (W = full rounds of tiles) are static round robin, the
+            // last tiles are handed out by the counter, each fetched one tile ahead, so CTAs that
+            // ran fast take the tail (VGG bucket n = 1: 84.7 -> 83.9 us; measured, all-dynamic
+            // schedules lose 13 %: the counter's latency under full HBM write traffic is exposed
+            // on every tile). Only with many short tiles (W >= 8): the BERT-L optimizer bucket
+            // (W = 3, ~5 us tiles) is 0.8 us slower with a dynamic tail.
+            const int waves = gp.num_tiles / nunits;
+            const int jst = dyn && waves >= 8 ? waves - EXP_DYN_WAVES : INT_MAX;   // static tiles per CTA
+            const int slim = jst == INT_MAX ? 0 : jst * nunits;       // first dynamic tile
+            int next = -1;
+            for (int j = 0;; ++j) {
+                int tile;
+                if (j < jst) {
+                    tile = unit + j * nunits;
+                    if (tile >= gp.num_tiles) tile = -1;
+                } else {
+                    tile = next < gp.num_tiles ? next : -1;
+                }
+                if (dyn) {
+                    const int r = j % SCHED_RING;
+                    if (j >= SCHED_RING) ptx::mbar_wait(sch_empty + 8 * r, ((j / SCHED_RING) - 1) & 1);
+                    sch[r] = tile;
+                    ptx::mbar_arrive(sch_full + 8 * r);
+                }
+                if (tile < 0) break;
+                // the following dynamic tile, fetched now: its latency overlaps this tile's loads
+                if (j + 1 >= jst) next = slim + static_cast<int>(atomicAdd(gp.sched, 1u));
                 const TileRef tr = locate<BN, CTAS>(gp, tile);
                 const LayerParams& Lp = gp.L[tr.li];
                 if (!(ready & (1u << tr.li))) {
@@ -500,6 +572,15 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
                     if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
                 }
             }
+            if (jst != INT_MAX) {
+                // this CTA's last fetch has returned: the last CTA to get here re-arms the
+                // counters for the next launch (stream order / griddepcontrol.wait keep launches apart)
+                __threadfence();
+                if (atomicAdd(gp.sched + 1, 1u) == gridDim.x - 1) {
+                    atomicExch(gp.sched, 0u);
+                    atomicExch(gp.sched + 1, 0u);
+                }
+            }
         }
     } else if (warp == 1) {
         // ===================================================== MMA issuer (one thread; the
@@ -509,7 +590,9 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = unit; tile < gp.num_tiles; tile += nunits) {
+            for (int j = 0;; ++j) {
+                const int tile = next_tile(j, false);
+                if (tile < 0) break;
                 const int nkb = gp.L[locate<BN, CTAS>(gp, tile).li].num_k_blocks;
                 ptx::mbar_wait(bar_tempty + 8 * acc, acc_phase ^ 1);   // epilogue drained it
                 ptx::tc_fence_after();
@@ -575,7 +658,9 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
         uint32_t acc_phase = 0;
         const float lr = gp.lr, mu = gp.mu, wd = gp.wd;
         const uint32_t tempty_leader = CTAS == 2 ? ptx::mapa(bar_tempty, 0) : bar_tempty;
-        for (int tile = unit; tile < gp.num_tiles; tile += nunits) {
+        for (int j = 0;; ++j) {
+            const int tile = next_tile(j, true);
+            if (tile < 0) break;
             const TileRef tr = locate<BN, CTAS>(gp, tile);
             // this tile's layer parameters, read once into registers
             const LayerParams& lp = gp.L[tr.li];
@@ -942,7 +1027,7 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
     if constexpr (CTAS == 2) ptx::cluster_sync();   // the leader's MMAs into the peer are done
     else __syncthreads();
     ptx::tc_fence_after();
-    if (FUSED && threadIdx.x == 0) DBG_STAMP(7);
+    if ((FUSED || EXP_END_STAMPS) && threadIdx.x == 0) DBG_STAMP(7);
     if (warp == 1) {
         if constexpr (CTAS == 2) ptx::tmem_dealloc_cg2<TMEM_COLS>(tmem_base);
         else ptx::tmem_dealloc<TMEM_COLS>(tmem_base);
@@ -1125,6 +1210,7 @@ tag_status_t launch_m(const ReconArgs* a, int count, cudaStream_t s, const Fused
     gp.mc_base = FUSED ? static_cast<char*>(fg->mc_base) : nullptr;
     gp.cast = FUSED && fg->cast ? 1 : 0;
     gp.local_ctr = FUSED ? fg->local_ctr : nullptr;
+    gp.sched = CTAS == 1 && !EXP_STATIC_SCHED ? a[0].sched : nullptr;
     auto kern = recon_tc_kernel<BN, CTAS, OUT_BF16, SGD, FUSED, X3, LONGK, MAXL>;
     // the shared-memory opt-in, once per instantiation and device (thread-safe)
     static std::atomic<uint64_t> attr_set{0};
@@ -1158,8 +1244,35 @@ tag_status_t launch_m(const ReconArgs* a, int count, cudaStream_t s, const Fused
         cudaMemcpyToSymbolAsync(g_dbg_stamps, zero, sizeof zero, 0, cudaMemcpyHostToDevice, s);
     }
 #endif
+#if EXP_END_STAMPS
+    {
+        static unsigned long long zero[160 * DBG_SLOTS];
+        cudaMemcpyToSymbolAsync(g_dbg_stamps, zero, sizeof zero, 0, cudaMemcpyHostToDevice, s);
+    }
+#endif
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, gp, npeers, me);
     if (e != cudaSuccess) return cuda_fail(e, "launch recon_tc_kernel");
+#if EXP_END_STAMPS
+    {
+        // diagnostics builds: how unevenly the persistent CTAs finish (us from the earliest start)
+        static unsigned long long st[160 * DBG_SLOTS];
+        cudaStreamSynchronize(s);
+        cudaMemcpyFromSymbol(st, g_dbg_stamps, sizeof st);
+        const int G = static_cast<int>(cfg.gridDim.x);
+        unsigned long long t0 = ~0ull;
+        for (int b = 0; b < G; ++b) t0 = st[b * DBG_SLOTS] < t0 ? st[b * DBG_SLOTS] : t0;
+        std::vector<double> s0, s7;
+        for (int b = 0; b < G; ++b) {
+            s0.push_back((st[b * DBG_SLOTS] - t0) / 1000.0);
+            s7.push_back((st[b * DBG_SLOTS + 7] - t0) / 1000.0);
+        }
+        std::sort(s0.begin(), s0.end());
+        std::sort(s7.begin(), s7.end());
+        std::fprintf(stderr, "[end stamps] grid %d tiles %d start max %.2f end min %.2f p10 %.2f "
+                     "p50 %.2f p90 %.2f max %.2f us\n", G, tiles, s0.back(), s7[0],
+                     s7[G / 10], s7[G / 2], s7[G * 9 / 10], s7.back());
+    }
+#endif
 #if EXP_FUSED_DBG == 3
     if (FUSED) {
         // diagnostics builds: phase stamps (max over CTAs, us from the earliest CTA start)

@@ -93,6 +93,9 @@ struct ReconArgs {
     uint64_t off_flag;     // the window flag area (WIN_* offsets)
     uint32_t* flags;       // the same area, this rank's device address
     int64_t cx, cy;        // elements of X_r / dY_r
+    // dynamic tile schedule counters (2 x u32, zero between launches; owned by the plan whose
+    // args are a[0]), or nullptr for the static schedule
+    uint32_t* sched;
 };
 
 struct FusedGather {

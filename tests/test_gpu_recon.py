@@ -705,3 +705,40 @@ def test_cuda_graph_capture_n1(tag, comm1, oracle_mod):
     g.close()
     for p in plans:
         p.close()
+
+
+def test_dynamic_tail_schedule_repeated_and_captured(tag, comm1, oracle_mod):
+    """Buckets of >= 8 rounds of one-CTA tiles hand their last two rounds out through a device
+    counter that the last CTA re-arms (recon_tc.cu): back-to-back launches, two plans interleaved
+    on one stream, and a CUDA graph of three launches replayed twice are all bit exact."""
+    M, N, K = 4096, 5120, 32             # 1280 tiles of 128 x 128: 8 rounds on 148 SMs
+    rs = np.random.default_rng(77)
+    X = rs.integers(-3, 4, (K, M)).astype(np.float32)
+    dY = rs.integers(-3, 4, (K, N)).astype(np.float32)
+    want = expected_int(oracle_mod, X, dY, K, "f32").view(np.uint32)
+    p1 = tag.SfbPlan(comm1, M, N, K, "bf16", "bf16", "f32")
+    p2 = tag.SfbPlan(comm1, M, N, K, "bf16", "bf16", "f32")
+    Xd, dYd = to_dev(X, "bf16"), to_dev(dY, "bf16")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    outs = [torch.full((M, N), float("nan"), device="cuda") for _ in range(4)]
+    with torch.cuda.stream(s):
+        for i in range(8):
+            (p1 if i % 2 == 0 else p2).sync(Xd, dYd, outs[i % 4], s)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), want)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        for i in range(3):
+            p1.sync(Xd, dYd, outs[i], s)
+    for _ in range(2):
+        for o in outs[:3]:
+            o.fill_(float("nan"))
+        with torch.cuda.stream(s):
+            g.replay()
+        torch.cuda.synchronize()
+        for o in outs[:3]:
+            assert np.array_equal(o.cpu().numpy().view(np.uint32), want)
+    p1.close()
+    p2.close()
