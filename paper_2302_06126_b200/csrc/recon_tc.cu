@@ -255,6 +255,8 @@ __device__ __forceinline__ void* mc_ptr(char* mc_base, ncclWindow_t w, size_t of
 constexpr int DBG_SLOTS = 8;
 __device__ unsigned long long g_dbg_stamps[160 * DBG_SLOTS];
 #define DBG_STAMP(slot) (g_dbg_stamps[blockIdx.x * DBG_SLOTS + (slot)] = gtimer())
+// a one-thread kernel launched right before / after the reconstruction (slot 1 / 2 of row 159)
+__global__ void dbg_marker_kernel(int slot) { g_dbg_stamps[159 * DBG_SLOTS + slot] = gtimer(); }
 #else
 #define DBG_STAMP(slot) ((void)0)
 #endif
@@ -422,6 +424,7 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
         return t;
     };
 
+    if (EXP_END_STAMPS && threadIdx.x == 0) DBG_STAMP(1);   // first instruction
     const uint32_t warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t crank = CTAS == 2 ? ptx::cluster_ctarank() : 0;   // 0 = leader of the pair
@@ -1229,14 +1232,22 @@ tag_status_t launch_m(const ReconArgs* a, int count, cudaStream_t s, const Fused
     cfg.dynamicSmemBytes = C::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see kernel)
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    attr[1].id = cudaLaunchAttributeClusterDimension;                  // CTA pair on one TPC
-    attr[1].val.clusterDim.x = CTAS;
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = 1;
+    int na = 0;
+#ifndef EXP_NO_PDL
+#define EXP_NO_PDL 0
+#endif
+    if (!EXP_NO_PDL) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // PDL (see kernel)
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (CTAS == 2) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;                  // CTA pair on one TPC
+        attr[na].val.clusterDim.x = CTAS;
+        attr[na].val.clusterDim.y = 1;
+        attr[na++].val.clusterDim.z = 1;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = CTAS == 2 ? 2 : 1;
+    cfg.numAttrs = na;
     const int npeers = FUSED ? fg->npeers : 1, me = FUSED ? fg->me : 0;
 #if EXP_FUSED_DBG == 3
     if (FUSED) {
@@ -1248,6 +1259,7 @@ tag_status_t launch_m(const ReconArgs* a, int count, cudaStream_t s, const Fused
     {
         static unsigned long long zero[160 * DBG_SLOTS];
         cudaMemcpyToSymbolAsync(g_dbg_stamps, zero, sizeof zero, 0, cudaMemcpyHostToDevice, s);
+        dbg_marker_kernel<<<1, 1, 0, s>>>(1);
     }
 #endif
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, gp, npeers, me);
@@ -1256,11 +1268,22 @@ tag_status_t launch_m(const ReconArgs* a, int count, cudaStream_t s, const Fused
     {
         // diagnostics builds: how unevenly the persistent CTAs finish (us from the earliest start)
         static unsigned long long st[160 * DBG_SLOTS];
+        dbg_marker_kernel<<<1, 1, 0, s>>>(2);
         cudaStreamSynchronize(s);
         cudaMemcpyFromSymbol(st, g_dbg_stamps, sizeof st);
         const int G = static_cast<int>(cfg.gridDim.x);
-        unsigned long long t0 = ~0ull;
-        for (int b = 0; b < G; ++b) t0 = st[b * DBG_SLOTS] < t0 ? st[b * DBG_SLOTS] : t0;
+        unsigned long long t0 = ~0ull, f0 = ~0ull, f1 = 0, e1 = 0;
+        for (int b = 0; b < G; ++b) {
+            t0 = st[b * DBG_SLOTS] < t0 ? st[b * DBG_SLOTS] : t0;
+            f0 = st[b * DBG_SLOTS + 1] < f0 ? st[b * DBG_SLOTS + 1] : f0;
+            f1 = st[b * DBG_SLOTS + 1] > f1 ? st[b * DBG_SLOTS + 1] : f1;
+            e1 = st[b * DBG_SLOTS + 7] > e1 ? st[b * DBG_SLOTS + 7] : e1;
+        }
+        const unsigned long long m1 = st[159 * DBG_SLOTS + 1], m2 = st[159 * DBG_SLOTS + 2];
+        std::fprintf(stderr, "[launch stamps] marker -> first CTA %.2f, CTA first instr spread %.2f, "
+                     "first instr -> body %.2f, body -> last end %.2f, last end -> marker %.2f, "
+                     "marker -> marker %.2f us\n", (f0 - m1) / 1e3, (f1 - f0) / 1e3, (t0 - f0) / 1e3,
+                     (e1 - t0) / 1e3, (m2 - e1) / 1e3, (m2 - m1) / 1e3);
         std::vector<double> s0, s7;
         for (int b = 0; b < G; ++b) {
             s0.push_back((st[b * DBG_SLOTS] - t0) / 1000.0);

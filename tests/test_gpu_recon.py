@@ -202,10 +202,12 @@ def test_local_grad_and_dense_n1(tag, comm1, oracle_mod):
     plan.close()
 
 
-@pytest.mark.parametrize("M,N,K,want", [(1024, 4096, 512, (128, 1)), (4096, 4096, 1024, (256, 2))])
+@pytest.mark.parametrize("M,N,K,want", [(1024, 4096, 512, (128, 1)), (4096, 4096, 1024, (256, 2)),
+                                         (4096, 5120, 32, (128, 1))])
 def test_fused_sgd_tile_configs_equal_unfused(tag, comm1, M, N, K, want):
     """E2 on both optimizer tile rules (128 x 128 tiles up to K = 512, CTA pairs with 64-row
-    stages above): fused == reconstruct + tag_sgd_step, bit for bit, over two steps."""
+    stages above; 4096 x 5120: 8 rounds of tiles, dynamic tail): fused == reconstruct +
+    tag_sgd_step, bit for bit, over two steps."""
     rs = np.random.default_rng(79)
     X = torch.from_numpy(rs.standard_normal((K, M)).astype(np.float32)).to(torch.bfloat16).cuda()
     dY = torch.from_numpy(rs.standard_normal((K, N)).astype(np.float32)).to(torch.bfloat16).cuda()
@@ -580,6 +582,7 @@ ADAM_HP = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
 
 
 @pytest.mark.parametrize("M,N,K,wire", [(4096, 1000, 32, "bf16"), (1024, 4096, 128, "bf16"),
+                                         (4096, 5120, 32, "bf16"),
                                          (4096, 4096, 256, "bf16"), (4096, 4096, 1024, "bf16"),
                                          (512, 1024, 32, "f32"),
                                          (130, 257, 10, "bf16"), (136, 264, 40, "bf16")])
