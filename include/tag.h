@@ -22,6 +22,10 @@
  *   - dtype of X / dY = desc.in_dtype; of dW_out = desc.out_dtype. W and v are always fp32.
  *   - Every call that takes a cudaStream_t is stream-ordered and asynchronous: it only enqueues
  *     work; inputs must stay unmodified and all buffers alive until the stream passes the call.
+ *   - One plan (or a group containing it) is used by one stream at a time: its gather buffers,
+ *     window call counter and the reconstruction's tile-schedule counters are per plan, so calls
+ *     on the same plan from two streams must be ordered (events) — different plans are
+ *     independent.
  *   - CUDA graphs: the calls keep no per-call state on the host. Which half of a plan's
  *     double-buffered symmetric window a gather fills, and the arrival-counter targets of the fused
  *     exchange, derive on the device from a call counter in the window, so tag_sfb_sync*, the group
