@@ -743,5 +743,19 @@ def test_dynamic_tail_schedule_repeated_and_captured(tag, comm1, oracle_mod):
         torch.cuda.synchronize()
         for o in outs[:3]:
             assert np.array_equal(o.cpu().numpy().view(np.uint32), want)
+    # two plans (own counters) running concurrently on two streams
+    s2 = torch.cuda.Stream()
+    s2.wait_stream(torch.cuda.current_stream())
+    for o in outs:
+        o.fill_(float("nan"))
+    torch.cuda.synchronize()
+    for i in range(6):
+        with torch.cuda.stream(s):
+            p1.sync(Xd, dYd, outs[i % 2], s)
+        with torch.cuda.stream(s2):
+            p2.sync(Xd, dYd, outs[2 + i % 2], s2)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert np.array_equal(o.cpu().numpy().view(np.uint32), want)
     p1.close()
     p2.close()
