@@ -752,6 +752,21 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
                             for (int i = 0; i < 8; ++i) hm[i] = __ldcs(mp4 + i * gs);
                         }
                     }
+#ifndef EXP_OPT_PF_NEXT
+#define EXP_OPT_PF_NEXT 1
+#endif
+                    if (EXP_OPT_PF_NEXT && CHUNKS >= 4 && ch + 1 < nch &&
+                        row0 + static_cast<int>(lane) < M) {
+                        // wide tiles (4 chunks per warp): the next chunk's rows (one 128-B line per
+                        // lane and array) into L2 as well, so its hoisted loads hit L2 (measured,
+                        // scripts/opt_epilogue_ab.py: BERT-L bucket at K = 8B SGD 42.0 -> 37.9 us,
+                        // Adam 62.5 -> 52.3; with 2 chunks per warp (K = B) no gain, Adam +2 us)
+                        const int64_t o = static_cast<int64_t>(row0 + lane) * N + n0 + half * GC +
+                                          (ch + 1) * COLS_PER_CHUNK;
+                        ptx::prefetch_l2(Wp + o);
+                        ptx::prefetch_l2(Vp + o);
+                        if (gp.opt == 2) ptx::prefetch_l2(lp.Mm + o);
+                    }
                     if (ch == 0) {
                         ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
                         ptx::tc_fence_after();
