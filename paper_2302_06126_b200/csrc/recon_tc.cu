@@ -767,6 +767,27 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
                         ptx::prefetch_l2(Vp + o);
                         if (gp.opt == 2) ptx::prefetch_l2(lp.Mm + o);
                     }
+#ifndef EXP_OPT_PF_TILE
+#define EXP_OPT_PF_TILE 1
+#endif
+                    if (EXP_OPT_PF_TILE && (CHUNKS >= 4 || gp.opt == 1) && ch + 1 == nch &&
+                        tile + nunits < gp.num_tiles) {
+                        // at a tile's last chunk: the first chunk rows of this unit's next tile in
+                        // the static order (with a dynamic tail the guess may miss; only a hint)
+                        // into L2. Measured (scripts/opt_epilogue_ab.py): BERT-L SGD at K = B
+                        // 30.9-31.7 -> 29.7 us, Adam at K = 8B 52.3 -> 50.2, Transformer SGD / Adam
+                        // at K = 8B 89 -> 87 / 120 -> 117; Adam on 2-chunk tiles +1-2 us (skipped)
+                        const TileRef nt = locate<BN, CTAS>(gp, tile + nunits);
+                        const LayerParams& nl = gp.L[nt.li];
+                        const int r = nt.m0 + static_cast<int>(crank) * BM + 32 * quad + static_cast<int>(lane);
+                        const int c0 = nt.n0 + half * GC;
+                        if (r < nl.M && c0 < nl.N) {
+                            const int64_t o = static_cast<int64_t>(r) * nl.N + c0;
+                            ptx::prefetch_l2(nl.W + o);
+                            ptx::prefetch_l2(nl.V + o);
+                            if (gp.opt == 2) ptx::prefetch_l2(nl.Mm + o);
+                        }
+                    }
                     if (ch == 0) {
                         ptx::mbar_wait(bar_tfull + 8 * acc, acc_phase);
                         ptx::tc_fence_after();
