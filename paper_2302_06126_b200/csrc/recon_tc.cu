@@ -411,13 +411,19 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
     volatile int* sch = reinterpret_cast<volatile int*>(gen_base + (s_sch - base));
     // the j-th tile of this CTA (-1: none left) for the MMA issuer (one thread) or an epilogue
     // warp (whole warp: every lane reads the slot before lane 0 frees it)
+    // dyn: the first W - EXP_DYN_WAVES rounds (W = full rounds of tiles) are static round robin
+    // and every role computes them itself; only the tail's tiles pass through the ring (index
+    // j - jst). Only with many short tiles (W >= 8; see the producer).
+    const int waves = gp.num_tiles / nunits;
+    const int jst = dyn && waves >= 8 ? waves - EXP_DYN_WAVES : INT_MAX;   // static tiles per CTA
     auto next_tile = [&](int j, bool whole_warp) -> int {
-        if (!dyn) {
+        if (j < jst) {
             const int t = unit + j * nunits;
             return t < gp.num_tiles ? t : -1;
         }
-        const int r = j % SCHED_RING;
-        ptx::mbar_wait(sch_full + 8 * r, (j / SCHED_RING) & 1);
+        const int jr = j - jst;
+        const int r = jr % SCHED_RING;
+        ptx::mbar_wait(sch_full + 8 * r, (jr / SCHED_RING) & 1);
         const int t = sch[r];
         if (whole_warp) __syncwarp();
         if (!whole_warp || ptx::lane_id() == 0) ptx::mbar_arrive(sch_empty + 8 * r);
@@ -483,8 +489,6 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
             // schedules lose 13 %: the counter's latency under full HBM write traffic is exposed
             // on every tile). Only with many short tiles (W >= 8): the BERT-L optimizer bucket
             // (W = 3, ~5 us tiles) is 0.8 us slower with a dynamic tail.
-            const int waves = gp.num_tiles / nunits;
-            const int jst = dyn && waves >= 8 ? waves - EXP_DYN_WAVES : INT_MAX;   // static tiles per CTA
             const int slim = jst == INT_MAX ? 0 : jst * nunits;       // first dynamic tile
             int next = -1;
             for (int j = 0;; ++j) {
@@ -495,9 +499,10 @@ recon_tc_kernel(const __grid_constant__ GroupParamsT<MAXL> gp, const int npeers,
                 } else {
                     tile = next < gp.num_tiles ? next : -1;
                 }
-                if (dyn) {
-                    const int r = j % SCHED_RING;
-                    if (j >= SCHED_RING) ptx::mbar_wait(sch_empty + 8 * r, ((j / SCHED_RING) - 1) & 1);
+                if (j >= jst) {
+                    const int jr = j - jst;
+                    const int r = jr % SCHED_RING;
+                    if (jr >= SCHED_RING) ptx::mbar_wait(sch_empty + 8 * r, ((jr / SCHED_RING) - 1) & 1);
                     sch[r] = tile;
                     ptx::mbar_arrive(sch_full + 8 * r);
                 }
