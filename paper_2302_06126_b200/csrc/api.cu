@@ -471,8 +471,10 @@ tag_status_t fused_sync(tag_plan_s* const* plans, int count, const void* const* 
         a[i].kbuf = p->win_kbuf;
         a[i].ctr = p->flags + WIN_CALLS / 4;
         a[i].ctr_mode = 2;
-        // no dynamic tail here (sched stays null): measured 1-2 us slower at n = 2 (102.4 vs
-        // 100.4-101.2 us, equal at n = 4; scripts/ab_fused_variants.sh)
+        // the dynamic tail schedule (recon_tc.cu): with only the tail's tiles passing through the
+        // smem ring, n = 2 / 4 fused steps 100.4 / 115.7-116.2 vs 100.5-100.8 / 117.8 us static
+        // (scripts/ab_fused_variants.sh)
+        a[i].sched = p->sched;
         a[i].C = dW[i];
         a[i].M = p->d.M;
         a[i].N = p->d.N;
