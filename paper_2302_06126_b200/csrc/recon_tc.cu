@@ -1170,13 +1170,19 @@ int use_ctas(const ReconArgs* a, int count) {
     return kmax >= 192 ? 2 : 1;
 }
 
-// Big (256 x 256 pair) tiles only when they fill every TPC at least once; a small-output bucket
+// Big (256 x 256 pair) tiles only when they fill at least half the TPCs; a small-output bucket
 // (e.g. Transformer FFN at K = 256: 16 pair tiles) runs faster on 4x as many 128 x 128 tiles.
+// Measured (scripts/recon_time.py): fc8 4096 x 1000 at K = 256 (64 pair tiles) 13.3 vs 15.3 us,
+// AlexNet / VGG-16 fc8 at K = 512 15.3 vs 19.4 us with big tiles from half a round (was: a full
+// round); fc7, FFN, out-proj unchanged.
 bool big_tiles(const ReconArgs* a, int count) {
     if (!use_wide(a, count)) return false;
     if (EXP_RECON_BN) return true;   // diagnostics builds force it
     const int ctas = use_ctas(a, count);
-    return tiles_for(a, count, 256, ctas) >= num_sms() / ctas;
+#ifndef EXP_BIG_FRAC
+#define EXP_BIG_FRAC 2   // big tiles from 1 / EXP_BIG_FRAC of a full round of units
+#endif
+    return tiles_for(a, count, 256, ctas) * EXP_BIG_FRAC >= num_sms() / ctas;
 }
 
 template <int BN, int CTAS, bool OUT_BF16, bool SGD, bool FUSED, bool X3, bool LONGK, int MAXL>
